@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py -- PMP iterations/s and time-to-1e-4 on BASELINE.json's config
+(configs[2]: 10M streams / 1M links, mixed log+linear utilities) on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One "step" is one full cold-start solve to eps_abs = 1e-4 (the time-to-
+tolerance half of the metric); ``value`` = total PMP iterations / total
+device time (CUDA events on the engine's stream, max over ranks), with the
+problem already resident in HBM.  ``e2e`` is the same metric through the
+C-ABI from pinned HOST buffers: problem upload + device CSR build + solve +
+solution download per step.  The reference arm times the reference's own
+CPU PmpSolver (oracle/_ref, compiled from /root/reference) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PMP iterations/sec and time-to-1e-4 residual, 10M streams, 1/2/4/8 B200"
+UNIT = "iterations/s"
+
+# BASELINE.json configs / SURVEY.md Appendix B (reference generators, fixed seeds)
+CONFIGS = {
+    "A": dict(m=1000, n=10000, avg=5.0, kind=0, uniform=False, seed=7, rho0=1000.0,
+              desc="A: 10k streams / 1k links, log, w=1"),
+    "B": dict(m=100000, n=1000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
+              desc="B: 1M streams / 100k links, log, w=1"),
+    "C": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0,
+              desc="C: 10M streams / 1M links, mixed log+linear (Bernoulli 0.5), w~U(0.5,1.5)"),
+    "D": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, degrade=(0.5, 0.5, 99),
+              desc="D: C with 50% of capacities x0.5 (degrade seed 99)"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_problem(name):
+    import paper_2509_10722_b200 as pmp
+
+    c = CONFIGS[name]
+    w = pmp.WeightDist.uniform(0.5, 1.5) if c["uniform"] else pmp.WeightDist.constant(1.0)
+    p = pmp.gen_uncongested(pmp.GenSpec(m=c["m"], n=c["n"], avg_links_per_stream=c["avg"],
+                                        kind=pmp.GenKind(c["kind"]), weights=w, seed=c["seed"]))
+    if "degrade" in c:
+        p = pmp.degrade(p, *c["degrade"])
+    return p
+
+
+def solver_config(name, max_iters=50000):
+    import paper_2509_10722_b200 as pmp
+
+    return pmp.SolverConfig(eps_abs=1e-4, rho0=CONFIGS[name]["rho0"], alpha=1.6, mu=2.0, gamma=1.1,
+                            rho_update_interval=50, max_iters=max_iters, trace_every=10)
+
+
+def alg_bytes(m, n, nnz):
+    """SURVEY.md 8(d) yardstick (fp64 values, int32 indices), per kernel."""
+    k1 = 4 * nnz + 4 * (n + 1) + n * (8 + 1 + 16 + 8) + 8 * m  # row_idx, col_ptr, w, kind, A r/w, x w, v gather
+    k2 = 4 * nnz + 4 * (m + 1) + 8 * n + m * (8 + 16 + 16 + 16 + 8)  # col_idx, row_ptr, x gather, c, price/B/zs r/w, v w
+    return k1, k2
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    return rank, world, local
+
+
+def barrier_sync(world):
+    import torch
+
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------- reference arm
+def reference_baseline(problem, name, iters, warmup=1):
+    """Time the reference CPU PmpSolver (oracle/_ref) on the same Problem.
+    Falls back to the plain-C restatement (1 core) if _ref is absent."""
+    from oracle import oracle as o
+
+    cores = os.cpu_count() or 1
+    cfg = o.Config(eps_abs=1e-4, rho0=CONFIGS[name]["rho0"], threads=cores)
+    if os.path.exists(o.REF_SO):
+        ref = o.Reference()
+        rp = ref.build_problem(problem.m, problem.n, problem.stream_offsets, problem.route_links, problem.kinds,
+                               problem.weights, problem.capacities)
+        sess = rp.bench_session(cfg)
+        if warmup:
+            sess.iterations(warmup)
+        secs = []
+        for _ in range(iters):
+            s, _ = sess.iterations(1)
+            secs.append(s)
+        sess.close()
+        kind = "reference"
+    else:
+        R = o.Restatement()
+        a = o.arrays_from(problem)
+        oc = o.Config(eps_abs=1e-4, rho0=CONFIGS[name]["rho0"])
+        st = R.cold_state(a, oc)
+        for _ in range(warmup):
+            R.step(a, oc, st)
+        secs = []
+        for _ in range(iters):
+            t = time.perf_counter()
+            R.step(a, oc, st)
+            secs.append(time.perf_counter() - t)
+        cores, kind = 1, "port"
+    return secs, cores, kind
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    name = args.config
+    problem = make_problem(name)
+    secs, cores, kind = reference_baseline(problem, name, args.steps, warmup=args.warmup)
+    total = float(sum(secs))
+    value = args.steps / total if total > 0 else None
+    sample = (f"{args.steps} timed iterations (+{args.warmup} warm-up) of the reference PmpSolver run loop "
+              f"(solver.hpp:450-476) from the cold state on config {name}; {cores} host threads")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator recipe, fixed seed)",
+        "config": {"workload": CONFIGS[name]["desc"], "m": problem.m, "n": problem.n, "nnz": problem.nnz,
+                   "eps_abs": 1e-4, "rho0": CONFIGS[name]["rho0"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import paper_2509_10722_b200 as pmp
+    from paper_2509_10722_b200 import _lib
+    from paper_2509_10722_b200.shard import ShardedPmpSolver, nccl_unique_id
+
+    rank, world, local = dist_setup(args)
+    name = args.config
+    t_gen = time.perf_counter()
+    problem = make_problem(name)
+    t_gen = time.perf_counter() - t_gen
+    cfg = solver_config(name)
+    L = _lib.lib()
+
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        solver = ShardedPmpSolver(problem, cfg, rank, world, obj[0], device=local)
+        h = solver.handle()
+    else:
+        solver = pmp.PmpSolver(problem, cfg, device=local)
+        h = solver.handle()
+
+    def check(rc):
+        if rc:
+            raise RuntimeError(L.numpmp_gpu_last_error(h).decode())
+
+    info = _lib.SolutionInfo()
+    ms = C.c_double()
+    # warm-up: full solves (graph instantiation, clocks)
+    for _ in range(args.warmup):
+        check(L.numpmp_gpu_set_cold(h))
+        check(L.numpmp_gpu_run_device(h, C.byref(info)))
+    check(L.numpmp_gpu_set_profiling(h, 1))
+    iters, dev_ms, statuses = [], [], []
+    with ClockSampler(local) as clocks:
+        barrier_sync(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            check(L.numpmp_gpu_set_cold(h))
+            check(L.numpmp_gpu_run_device(h, C.byref(info)))
+            check(L.numpmp_gpu_last_run_ms(h, C.byref(ms)))
+            iters.append(int(info.iterations))
+            statuses.append(int(info.status))
+            dev_ms.append(ms.value)
+        barrier_sync(world)
+        wall = time.perf_counter() - t0
+    launches, ms1, ms2, it_t = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
+    check(L.numpmp_gpu_profile(h, C.byref(launches), C.byref(ms1), C.byref(ms2), C.byref(it_t)))
+    check(L.numpmp_gpu_set_profiling(h, 0))
+    total_ms = max_over_ranks(world, float(sum(dev_ms)))
+    total_iters = int(sum(iters))
+    value = total_iters / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # roofline of the dominant kernel (per launch, this rank's shard)
+    lp = solver.local if world > 1 else problem
+    k1b, k2b = alg_bytes(lp.m, lp.n, lp.nnz)
+    n_it = max(int(it_t.value), 1)
+    avg1, avg2 = ms1.value / n_it, ms2.value / n_it
+    hbm, peak_kind = peaks()
+    if avg2 >= avg1:
+        dom, dom_bytes, dom_ms = "k_link_pass (R.x gather + link epilogue + finalize)", k2b, avg2
+    else:
+        dom, dom_bytes, dom_ms = "k_stream_pass (R^T.v gather + prox)", k1b, avg1
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    iter_ms = (ms1.value + ms2.value) / n_it
+    iter_gbs = (k1b + k2b) / (iter_ms * 1e-3) / 1e9
+
+    # e2e: the public C-ABI from pinned host buffers, per step:
+    # create (H2D problem + device CSR build) -> solve -> D2H solution -> destroy
+    e2e = None
+    if world == 1:
+        arrays = [problem.capacities, problem.weights, problem.kinds, problem.stream_offsets, problem.route_links]
+        for a in arrays:
+            check(L.numpmp_gpu_pin_host(_lib.ptr(a), a.nbytes))
+        x = np.empty(problem.n)
+        s = np.empty(problem.m)
+        lam = np.empty(problem.m)
+        lraw = np.empty(problem.m)
+        outs = [x, s, lam, lraw]
+        for a in outs:
+            check(L.numpmp_gpu_pin_host(_lib.ptr(a), a.nbytes))
+        h2d = sum(a.nbytes for a in arrays)
+        d2h = sum(a.nbytes for a in outs)
+        cap = cfg.max_iters // cfg.trace_every + 2
+        trace = (_lib.TraceRow * cap)()
+        e_iters, e_secs = [], []
+        solver_e2e = None
+        for step in range(args.steps + 1):  # first is warm-up
+            import torch
+
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            hh = C.c_void_p()
+            view = problem.view()
+            check(L.numpmp_gpu_create(C.byref(view), C.byref(cfg._c()), local, C.byref(hh)))
+            rc = L.numpmp_gpu_run(hh, _lib.ptr(x), _lib.ptr(s), _lib.ptr(lam), _lib.ptr(lraw), C.byref(info), trace, cap)
+            L.numpmp_gpu_destroy(hh)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t
+            if rc:
+                raise RuntimeError("e2e run failed")
+            if step > 0:
+                e_iters.append(int(info.iterations))
+                e_secs.append(el)
+        for a in arrays + outs:
+            L.numpmp_gpu_unpin_host(_lib.ptr(a))
+        e2e = {"value": sum(e_iters) / sum(e_secs), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * sum(e_secs) / len(e_secs),
+               "timing": "host wall clock around create+solve+download+destroy, synchronized"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        secs, cores, kind = reference_baseline(problem, name, args.cpu_iters, warmup=1)
+        cpu = {"value": len(secs) / sum(secs), "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{len(secs)} iterations (+1 warm-up) of the reference run loop on config {name}, "
+                         f"{cores} host threads ({'oracle/_ref = reference headers compiled -O3' if kind == 'reference' else 'oracle restatement, 1 core'})"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator recipe gen_uncongested, fixed seed; regenerated bit-exactly)",
+            "config": {"workload": CONFIGS[name]["desc"], "m": problem.m, "n": problem.n, "nnz": problem.nnz,
+                       "eps_abs": 1e-4, "rho0": CONFIGS[name]["rho0"], "alpha": 1.6,
+                       "parallelism": f"stream shards x{world}" + (" + NCCL all-reduce of link loads" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (>1.3 GB touched per iteration vs 126 MB L2)",
+                       "step": "one cold-start solve to eps_abs=1e-4 (time-to-tolerance)"},
+            "iterations_per_solve": iters, "status": statuses,
+            "time_to_tol_s": ms_per_step / 1e3,
+            "ms_per_iteration": total_ms / max(total_iters, 1),
+            "wall_s_timed": wall,
+            "gen_s": t_gen,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                         "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms},
+            "iteration_roofline": {"alg_bytes": k1b + k2b, "ms": iter_ms, "achieved_gbs": iter_gbs,
+                                   "frac": iter_gbs / hbm, "stream_pass_ms": avg1, "link_pass_ms": avg2},
+            "gpu_launches": int(launches.value) + args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,70 @@
+/*
+ * numpmp_host.h -- host-side C-ABI of libnumpmp_cuda.so: synthetic instance
+ * generation, problem validation and the reference layout, all on the host
+ * (no device work).  These are the input producers of the hot path; each
+ * restates one reference function so the same seed gives the bit-identical
+ * Problem (checked against the reference in tests/test_host.py):
+ *
+ *   numpmp_gen_uncongested  gen.hpp:61-97 + rng.hpp:17-77
+ *   numpmp_gen_congested    gen.hpp:103-128
+ *   numpmp_degrade          gen.hpp:132-143
+ *   numpmp_validate         model.hpp:76-155 (+ violations_message 203-215)
+ *   numpmp_build_layout     model.hpp:159-201
+ */
+#ifndef NUMPMP_HOST_H_
+#define NUMPMP_HOST_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GenSpec (gen.hpp:35-44). kind: 0 log, 1 linear, 2 mixed (GenKind);
+ * weight_kind: 0 constant(weight_a), 1 uniform(weight_a, weight_b). */
+typedef struct {
+  int64_t m;
+  int64_t n; /* 0 -> max(1, m/2) */
+  double avg_links_per_stream;
+  int32_t kind;
+  int32_t weight_kind;
+  double weight_a;
+  double weight_b;
+  uint64_t seed;
+} numpmp_gen_spec;
+
+/* A generated instance owned by the library (stream-major incidence). */
+typedef struct numpmp_instance numpmp_instance;
+
+/* Returns 0, or 5 (GenError) / 2 (ValidationError) with a message in
+ * numpmp_host_last_error(). */
+int numpmp_gen_uncongested(const numpmp_gen_spec* spec, numpmp_instance** out);
+int numpmp_gen_congested(const numpmp_gen_spec* spec, double hot_link_fraction,
+                         double hot_stream_fraction, numpmp_instance** out);
+void numpmp_instance_sizes(const numpmp_instance* inst, int64_t* m, int64_t* n, int64_t* nnz);
+/* Copies the instance out; any pointer may be null. */
+void numpmp_instance_export(const numpmp_instance* inst, double* capacities, double* weights,
+                            uint8_t* kinds, int64_t* stream_offsets, int32_t* route_links);
+void numpmp_instance_free(numpmp_instance* inst);
+
+/* In-place capacity degradation with the reference's draw order. */
+int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor, uint64_t seed);
+
+/* Model validation; returns the number of violations and writes the
+ * reference's "invalid problem: [...]" message (truncated to msg_cap). */
+int64_t numpmp_validate(int64_t m, int64_t n, const double* capacities, const double* weights,
+                        const uint8_t* kinds, const int64_t* stream_offsets,
+                        const int32_t* route_links, char* msg, int64_t msg_cap);
+
+/* The reference TerminalLayout on the host (terminal_link[J],
+ * link_offsets[m+1], link_terminals[J], link_counts[m]). */
+int numpmp_build_layout(int64_t m, int64_t n, const int64_t* stream_offsets,
+                        const int32_t* route_links, int32_t* terminal_link,
+                        int64_t* link_offsets, int64_t* link_terminals, int32_t* link_counts);
+
+const char* numpmp_host_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NUMPMP_HOST_H_ */

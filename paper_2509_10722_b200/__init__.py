@@ -1,0 +1,47 @@
+"""paper_2509_10722_b200 -- B200-native (sm_100a) proximal message passing
+(PMP / over-relaxed ADMM) for network utility maximization.
+
+A drop-in for the reference numpmp engine's hot path
+(proj/include/numpmp/solver.hpp:265-519): the same Problem / SolverConfig /
+SolverState / Solution types and PmpSolver members, with every iteration
+running as hand-written CUDA kernels behind the C-ABI in
+include/numpmp_gpu.h.
+"""
+from .errors import DeviceError, DomainError, GenError, SolverError, ValidationError
+from .model import (
+    GenKind,
+    GenSpec,
+    Problem,
+    Stream,
+    StreamKind,
+    TerminalLayout,
+    WeightDist,
+    build_problem,
+    degrade,
+    gen_congested,
+    gen_uncongested,
+    problem_from_arrays,
+    validate,
+)
+from .solver import (
+    PmpSolver,
+    Solution,
+    SolverConfig,
+    SolverState,
+    SolveStatus,
+    TraceRecord,
+    WarmStart,
+    check_termination,
+    objective,
+    recover_duals,
+    to_string,
+    update_rho,
+)
+
+__all__ = [
+    "DeviceError", "DomainError", "GenError", "SolverError", "ValidationError",
+    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "WeightDist",
+    "build_problem", "degrade", "gen_congested", "gen_uncongested", "problem_from_arrays", "validate",
+    "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
+    "check_termination", "objective", "recover_duals", "to_string", "update_rho",
+]

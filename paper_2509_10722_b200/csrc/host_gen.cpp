@@ -1,0 +1,349 @@
+// host_gen.cpp -- host-side input producers of the PMP hot path (no device
+// work): synthetic instances, validation and the reference terminal layout.
+//
+// Each function restates one reference function so the same spec and seed
+// give the bit-identical Problem (tests/test_host.py compares every array
+// with the reference's own generator):
+//   Rng                 rng.hpp:17-77  (mt19937_64 raw output is pinned by
+//                                       the standard; hand-rolled draws)
+//   gen_uncongested     gen.hpp:61-97
+//   gen_congested       gen.hpp:103-128
+//   degrade             gen.hpp:132-143
+//   validate            model.hpp:76-155, violations_message 203-215
+//   build_layout        model.hpp:159-201
+//
+// Unlike the reference, instances are produced directly in the compact
+// stream-major CSC form the device consumes (offsets + route links), with
+// no per-stream heap objects: generation of config C (10M streams, 100M
+// nonzeros) is bound by the sequential mt19937_64 stream only.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "numpmp_host.h"
+
+namespace {
+
+thread_local std::string g_host_err;
+
+// rng.hpp:17-77, draw for draw.
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : eng_(seed) {}
+  std::uint64_t next_u64() { return eng_(); }
+  double uniform01() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  double uniform(double a, double b) { return a + (b - a) * uniform01(); }
+  bool bernoulli(double p) { return uniform01() < p; }
+  std::uint64_t uniform_u64(std::uint64_t n) {
+    const std::uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    std::uint64_t r;
+    do {
+      r = next_u64();
+    } while (r >= limit);
+    return r % n;
+  }
+  std::int64_t uniform_int(std::int64_t n) {
+    return static_cast<std::int64_t>(uniform_u64(static_cast<std::uint64_t>(n)));
+  }
+  // Knuth's product method with the limit exp(-lambda) hoisted by the caller
+  // (the reference recomputes the same value on every call).
+  std::int64_t poisson(double lambda, double limit) {
+    if (lambda <= 0.0) return 0;
+    std::int64_t k = 0;
+    double prod = 1.0;
+    do {
+      ++k;
+      prod *= uniform01();
+    } while (prod > limit);
+    return k - 1;
+  }
+  // Floyd's algorithm, then sorted ascending.  The chosen-set is only
+  // queried for membership, so a linear scan over the (short) output is
+  // equivalent to the reference's unordered_set.
+  void sample_without_replacement(std::int64_t n, std::int64_t k, std::int32_t* out) {
+    if (k <= 64) {
+      for (std::int64_t j = n - k, c = 0; j < n; ++j, ++c) {
+        std::int64_t t = uniform_int(j + 1);
+        for (std::int64_t q = 0; q < c; ++q)
+          if (out[q] == t) {
+            t = j;
+            break;
+          }
+        out[c] = static_cast<std::int32_t>(t);
+      }
+    } else {
+      std::unordered_set<std::int64_t> chosen;
+      for (std::int64_t j = n - k, c = 0; j < n; ++j, ++c) {
+        std::int64_t t = uniform_int(j + 1);
+        if (chosen.count(t)) t = j;
+        chosen.insert(t);
+        out[c] = static_cast<std::int32_t>(t);
+      }
+    }
+    std::sort(out, out + k);
+  }
+
+ private:
+  std::mt19937_64 eng_;
+};
+
+}  // namespace
+
+struct numpmp_instance {
+  std::int64_t m = 0, n = 0;
+  std::vector<double> capacities, weights;
+  std::vector<std::uint8_t> kinds;
+  std::vector<std::int64_t> offsets;
+  std::vector<std::int32_t> routes;
+};
+
+namespace {
+
+int check_spec(const numpmp_gen_spec* s, std::int64_t* n_out) {
+  // gen.hpp:43, 48-56
+  const std::int64_t n = s->n > 0 ? s->n : std::max<std::int64_t>(1, s->m / 2);
+  if (s->m < 1) {
+    g_host_err = "generator spec: m must be >= 1";
+    return 5;
+  }
+  if (!(s->avg_links_per_stream >= 1.0)) {
+    g_host_err = "generator spec: avg_links_per_stream must be >= 1";
+    return 5;
+  }
+  if (s->weight_kind == 1 && !(s->weight_a <= s->weight_b)) {
+    g_host_err = "generator spec: weight range inverted";
+    return 5;
+  }
+  if (s->m > INT32_MAX) {
+    g_host_err = "generator spec: m exceeds the int32 link id range";
+    return 5;
+  }
+  *n_out = n;
+  return 0;
+}
+
+// gen.hpp:61-85: per stream (route length, links, kind, weight), then per
+// link capacity.
+void draw(const numpmp_gen_spec* s, std::int64_t n, Rng& rng, numpmp_instance* inst) {
+  inst->m = s->m;
+  inst->n = n;
+  inst->weights.resize(static_cast<std::size_t>(n));
+  inst->kinds.resize(static_cast<std::size_t>(n));
+  inst->offsets.assign(static_cast<std::size_t>(n) + 1, 0);
+  const double lambda = s->avg_links_per_stream - 1.0;
+  const double limit = std::exp(-lambda);
+  inst->routes.reserve(static_cast<std::size_t>(
+      static_cast<double>(n) * s->avg_links_per_stream * 1.01 + 64));
+  std::vector<std::int32_t> tmp;
+  for (std::int64_t j = 0; j < n; ++j) {
+    std::int64_t len = 1 + rng.poisson(lambda, limit);
+    if (len > s->m) len = s->m;
+    const std::size_t base = inst->routes.size();
+    inst->routes.resize(base + static_cast<std::size_t>(len));
+    rng.sample_without_replacement(s->m, len, inst->routes.data() + base);
+    inst->offsets[static_cast<std::size_t>(j) + 1] = static_cast<std::int64_t>(inst->routes.size());
+    std::uint8_t kind = static_cast<std::uint8_t>(s->kind == 2 ? 0 : s->kind);
+    if (s->kind == 2) kind = rng.bernoulli(0.5) ? 0 : 1;
+    inst->kinds[static_cast<std::size_t>(j)] = kind;
+    inst->weights[static_cast<std::size_t>(j)] =
+        s->weight_kind == 0 ? s->weight_a : rng.uniform(s->weight_a, s->weight_b);
+  }
+  inst->capacities.resize(static_cast<std::size_t>(s->m));
+  for (double& c : inst->capacities) c = rng.uniform(0.5, 1.5);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* numpmp_host_last_error(void) { return g_host_err.c_str(); }
+
+int numpmp_gen_uncongested(const numpmp_gen_spec* spec, numpmp_instance** out) {
+  std::int64_t n = 0;
+  if (int rc = check_spec(spec, &n)) return rc;
+  try {
+    auto* inst = new numpmp_instance();
+    Rng rng(spec->seed);
+    draw(spec, n, rng, inst);
+    *out = inst;
+    return 0;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return 9;
+  }
+}
+
+int numpmp_gen_congested(const numpmp_gen_spec* spec, double hot_link_fraction,
+                         double hot_stream_fraction, numpmp_instance** out) {
+  std::int64_t n = 0;
+  if (int rc = check_spec(spec, &n)) return rc;
+  if (!(hot_link_fraction > 0.0 && hot_link_fraction <= 1.0)) {
+    g_host_err = "hot_link_fraction must be in (0, 1]";
+    return 5;
+  }
+  if (!(hot_stream_fraction > 0.0 && hot_stream_fraction <= 1.0)) {
+    g_host_err = "hot_stream_fraction must be in (0, 1]";
+    return 5;
+  }
+  try {
+    numpmp_instance base;
+    Rng rng(spec->seed);
+    draw(spec, n, rng, &base);
+    // gen.hpp:115-126: each hot link joins a Bernoulli subset of streams,
+    // inserted in sorted position unless already present.
+    const std::int64_t hot_count =
+        static_cast<std::int64_t>(std::ceil(hot_link_fraction * static_cast<double>(spec->m)));
+    const std::int64_t k = std::min(hot_count, spec->m);
+    std::vector<std::int32_t> hot(static_cast<std::size_t>(k));
+    rng.sample_without_replacement(spec->m, k, hot.data());
+    std::vector<std::vector<std::int32_t>> routes(static_cast<std::size_t>(n));
+    for (std::int64_t j = 0; j < n; ++j)
+      routes[static_cast<std::size_t>(j)].assign(base.routes.begin() + base.offsets[j],
+                                                 base.routes.begin() + base.offsets[j + 1]);
+    for (std::int32_t link : hot) {
+      for (auto& r : routes) {
+        if (!rng.bernoulli(hot_stream_fraction)) continue;
+        if (std::binary_search(r.begin(), r.end(), link)) continue;
+        r.insert(std::upper_bound(r.begin(), r.end(), link), link);
+      }
+    }
+    auto* inst = new numpmp_instance();
+    inst->m = base.m;
+    inst->n = base.n;
+    inst->capacities = std::move(base.capacities);
+    inst->weights = std::move(base.weights);
+    inst->kinds = std::move(base.kinds);
+    inst->offsets.assign(static_cast<std::size_t>(n) + 1, 0);
+    for (std::int64_t j = 0; j < n; ++j) {
+      const auto& r = routes[static_cast<std::size_t>(j)];
+      inst->routes.insert(inst->routes.end(), r.begin(), r.end());
+      inst->offsets[static_cast<std::size_t>(j) + 1] = static_cast<std::int64_t>(inst->routes.size());
+    }
+    *out = inst;
+    return 0;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return 9;
+  }
+}
+
+void numpmp_instance_sizes(const numpmp_instance* inst, int64_t* m, int64_t* n, int64_t* nnz) {
+  *m = inst->m;
+  *n = inst->n;
+  *nnz = static_cast<int64_t>(inst->routes.size());
+}
+
+void numpmp_instance_export(const numpmp_instance* inst, double* capacities, double* weights,
+                            uint8_t* kinds, int64_t* stream_offsets, int32_t* route_links) {
+  if (capacities) std::memcpy(capacities, inst->capacities.data(), 8 * inst->capacities.size());
+  if (weights) std::memcpy(weights, inst->weights.data(), 8 * inst->weights.size());
+  if (kinds) std::memcpy(kinds, inst->kinds.data(), inst->kinds.size());
+  if (stream_offsets) std::memcpy(stream_offsets, inst->offsets.data(), 8 * inst->offsets.size());
+  if (route_links) std::memcpy(route_links, inst->routes.data(), 4 * inst->routes.size());
+}
+
+void numpmp_instance_free(numpmp_instance* inst) { delete inst; }
+
+int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor,
+                   uint64_t seed) {
+  // gen.hpp:132-143
+  if (!(p_degrade >= 0.0 && p_degrade <= 1.0)) {
+    g_host_err = "degrade: probability must be in [0, 1]";
+    return 5;
+  }
+  if (!(factor > 0.0 && factor <= 1.0)) {
+    g_host_err = "degrade: factor must be in (0, 1]";
+    return 5;
+  }
+  Rng rng(seed);
+  for (int64_t l = 0; l < m; ++l)
+    if (rng.bernoulli(p_degrade)) capacities[l] *= factor;
+  return 0;
+}
+
+int64_t numpmp_validate(int64_t m, int64_t n, const double* capacities, const double* weights,
+                        const uint8_t* kinds, const int64_t* offsets, const int32_t* routes,
+                        char* msg, int64_t msg_cap) {
+  // model.hpp:76-135 (the layout block 137-153 holds by construction here).
+  struct V {
+    std::string rule, message;
+  };
+  std::vector<V> vs;
+  if (m <= 0) vs.push_back({"link-count", "m must be >= 1"});
+  if (n <= 0) vs.push_back({"stream-count", "n must be >= 1"});
+  char buf[256];
+  for (int64_t i = 0; i < m; ++i) {
+    const double c = capacities[i];
+    if (!(c > 0.0) || !std::isfinite(c)) {
+      std::snprintf(buf, sizeof buf, "link %lld has non-positive capacity %g", (long long)i, c);
+      vs.push_back({"positive-capacity", buf});
+    }
+  }
+  std::vector<std::int32_t> sorted;
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t b = offsets[j], e = offsets[j + 1];
+    if (e <= b) vs.push_back({"non-empty-route", "route must contain a link"});
+    sorted.assign(routes + b, routes + (e > b ? e : b));
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) {
+      std::snprintf(buf, sizeof buf, "stream %lld visits a link twice", (long long)j);
+      vs.push_back({"distinct-links", buf});
+    }
+    for (int64_t t = b; t < e; ++t) {
+      const std::int32_t link = routes[t];
+      if (link < 0 || int64_t(link) >= m) {
+        std::snprintf(buf, sizeof buf, "stream %lld references link %d outside [0, %lld)",
+                      (long long)j, link, (long long)m);
+        vs.push_back({"link-in-range", buf});
+      }
+    }
+    const double w = weights[j];
+    if (!std::isfinite(w)) {
+      vs.push_back({"finite-weight", "weight must be finite"});
+    } else if (kinds[j] == 0) {
+      if (!(w > 0.0)) vs.push_back({"positive-log-weight", "log-utility stream requires weight > 0"});
+    } else {
+      if (w < 0.0) vs.push_back({"nonnegative-weight", "weight must be >= 0"});
+    }
+  }
+  // violations_message, model.hpp:203-215
+  std::string out = "invalid problem:";
+  std::size_t shown = 0;
+  for (const V& v : vs) {
+    if (shown++ == 8) {
+      out += " ... (" + std::to_string(vs.size() - 8) + " more)";
+      break;
+    }
+    out += " [" + v.rule + ": " + v.message + "]";
+  }
+  if (msg && msg_cap > 0) {
+    std::strncpy(msg, out.c_str(), static_cast<std::size_t>(msg_cap) - 1);
+    msg[msg_cap - 1] = 0;
+  }
+  return static_cast<int64_t>(vs.size());
+}
+
+int numpmp_build_layout(int64_t m, int64_t n, const int64_t* offsets, const int32_t* routes,
+                        int32_t* terminal_link, int64_t* link_offsets, int64_t* link_terminals,
+                        int32_t* link_counts) {
+  // model.hpp:159-201
+  const int64_t nnz = offsets[n];
+  const int64_t J = nnz + m;
+  std::memcpy(terminal_link, routes, 4 * static_cast<std::size_t>(nnz));
+  for (int64_t l = 0; l < m; ++l) terminal_link[nnz + l] = static_cast<int32_t>(l);
+  std::fill(link_counts, link_counts + m, 0);
+  for (int64_t t = 0; t < J; ++t) ++link_counts[terminal_link[t]];
+  link_offsets[0] = 0;
+  for (int64_t l = 0; l < m; ++l) link_offsets[l + 1] = link_offsets[l] + link_counts[l];
+  std::vector<int64_t> cursor(link_offsets, link_offsets + m);
+  for (int64_t t = 0; t < J; ++t) link_terminals[cursor[terminal_link[t]]++] = t;
+  return 0;
+}
+
+}  // extern "C"

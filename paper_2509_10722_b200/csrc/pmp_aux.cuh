@@ -1,0 +1,180 @@
+// pmp_aux.cuh -- setup / state-materialisation / post-processing kernels.
+// None of these run inside the iteration loop.
+#pragma once
+
+#include "pmp_kernels.cuh"
+
+namespace numpmp_dev {
+
+// int64 stream offsets -> int32 CSC column pointer (nnz < 2^31 checked on host).
+__global__ void k_offsets_to_i32(const long long* __restrict__ in, int* __restrict__ out,
+                                 long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = static_cast<int>(in[i]);
+}
+
+// terminal -> stream map and terminal iota (sort values).
+__global__ void k_terminal_stream(const int* __restrict__ col_ptr, long long n,
+                                  int* __restrict__ t2s) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const int b = col_ptr[j], e = col_ptr[j + 1];
+    for (int t = b; t < e; ++t) t2s[t] = static_cast<int>(j);
+  }
+}
+__global__ void k_iota(int* __restrict__ out, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = static_cast<int>(i);
+}
+// Row pointer from the link-sorted keys: row_ptr[l] = first k with key >= l.
+__global__ void k_row_ptr_from_sorted(const int* __restrict__ keys, long long nnz, long long m,
+                                      int* __restrict__ row_ptr) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= nnz;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int cur = (k < nnz) ? keys[k] : static_cast<int>(m);
+    const int prev = (k > 0) ? keys[k - 1] : -1;
+    for (int l = prev + 1; l <= cur; ++l) row_ptr[l] = static_cast<int>(k);
+  }
+}
+__global__ void k_gather_i32(const int* __restrict__ src, const int* __restrict__ idx,
+                             int* __restrict__ out, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+__global__ void k_degree(const int* __restrict__ row_ptr, long long m, int* __restrict__ deg) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x)
+    deg[l] = row_ptr[l + 1] - row_ptr[l];
+}
+
+// Sequential per-row sums L_l = sum_{j in row l} src_j (ascending stream
+// order) -- the same arithmetic as the link pass.
+__global__ void __launch_bounds__(kThreads) k_row_sums(const int* __restrict__ row_ptr,
+                                                       const int* __restrict__ col_idx,
+                                                       const double* __restrict__ src, long long m,
+                                                       double* __restrict__ out) {
+  __shared__ double sbuf[kWarps][kChunk];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  const long long ngroups = (m + 31) / 32;
+  for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
+       g += (long long)gridDim.x * kWarps) {
+    const long long r = g * 32 + lane;
+    const bool valid = r < m;
+    const int rb = row_ptr[valid ? r : m];
+    const int re = valid ? row_ptr[r + 1] : rb;
+    const int sb = __shfl_sync(kFull, rb, 0), se = __shfl_sync(kFull, re, 31);
+    const double L = warp_segmented_sum(col_idx, sb, se, rb, re, sbuf[wib], lane, GatherX{src}, pol);
+    if (valid) out[r] = L;
+  }
+}
+
+// warm_start_from (solver.hpp:218-259) in link space, given L = R x0:
+// slack = max(c - L, 0); ps = slack - c; pbar = (L + ps)/(d+1);
+// A = x0 (done by the caller), B = pbar, zs = ps - pbar, Q = L.
+__global__ void k_warm_links(const double* __restrict__ L, const int* __restrict__ deg,
+                             const int* __restrict__ row_ptr, const double* __restrict__ cap,
+                             long long m, double* __restrict__ B, double* __restrict__ zs,
+                             double* __restrict__ Q, double* __restrict__ ps0,
+                             double* __restrict__ pbar0) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double c = cap[l];
+    const double load = L[l];
+    const double slack = dmax_ref(c - load, 0.0);
+    const double ps = slack - c;
+    const int d = deg ? deg[l] : row_ptr[l + 1] - row_ptr[l];
+    const double pbar = (load + ps) / static_cast<double>(d + 1);
+    B[l] = pbar;
+    zs[l] = ps - pbar;
+    Q[l] = load;
+    ps0[l] = ps;
+    pbar0[l] = pbar;
+  }
+}
+
+// Link part of state materialisation after >= 1 iteration: the slack flow
+// and link average of the last iteration, recomputed with the identical
+// arithmetic from the previous-iterate buffers.
+__global__ void k_materialize_links(const double* __restrict__ L, const int* __restrict__ deg,
+                                    const int* __restrict__ row_ptr,
+                                    const double* __restrict__ cap,
+                                    const double* __restrict__ zs_prev,
+                                    const double* __restrict__ pr_prev, double rho_iter,
+                                    long long m, double* __restrict__ ps,
+                                    double* __restrict__ pbar) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double u = pr_prev[l] / rho_iter;
+    const double p = dmax_ref(zs_prev[l] - u, -cap[l]);
+    const int d = deg ? deg[l] : row_ptr[l + 1] - row_ptr[l];
+    ps[l] = p;
+    pbar[l] = (L[l] + p) / static_cast<double>(d + 1);
+  }
+}
+
+// Terminal-space expansion: p_t = x_j, z_t = A_j - B_l (and the previous
+// iterate's copies) for traffic terminals.
+__global__ void k_expand_terminals(const int* __restrict__ col_ptr, const int* __restrict__ row_idx,
+                                   long long n, const double* __restrict__ x,
+                                   const double* __restrict__ A, const double* __restrict__ B,
+                                   const double* __restrict__ A_prev,
+                                   const double* __restrict__ B_prev, double* __restrict__ p,
+                                   double* __restrict__ z, double* __restrict__ z_prev) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const int b = col_ptr[j], e = col_ptr[j + 1];
+    for (int t = b; t < e; ++t) {
+      const int l = row_idx[t];
+      if (p) p[t] = x[j];
+      if (z) z[t] = A[j] - B[l];
+      if (z_prev) z_prev[t] = A_prev[j] - B_prev[l];
+    }
+  }
+}
+
+// Post-processing (solver.hpp:483-504): x clamp of tiny negatives, lambda,
+// lambda_raw; objective partials (clamped for Solution.objective,
+// unclamped for the final trace row).
+__global__ void __launch_bounds__(kThreads) k_post_streams(const double* __restrict__ x,
+                                                           const double* __restrict__ w,
+                                                           const unsigned char* __restrict__ kind,
+                                                           long long n, double eps_abs,
+                                                           double* __restrict__ x_sol,
+                                                           double* __restrict__ part) {
+  double v[2] = {0.0, 0.0};
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const double xj = x[j];
+    const double xc = (xj < 0.0 && -xj < eps_abs) ? 0.0 : xj;
+    x_sol[j] = xc;
+    const bool lg = kind[j] == NUMPMP_KIND_LOG;
+    v[0] += lg ? w[j] * log(xc) : w[j] * xc;
+    v[1] += lg ? w[j] * log(xj) : w[j] * xj;
+  }
+  block_sum_store<2>(v, part + 2 * blockIdx.x);
+}
+__global__ void k_post_links(const double* __restrict__ L, const double* __restrict__ cap,
+                             const double* __restrict__ price, long long m,
+                             double* __restrict__ s, double* __restrict__ lambda) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    s[l] = dmax_ref(cap[l] - L[l], 0.0);
+    lambda[l] = dmax_ref(price[l], 0.0);
+  }
+}
+__global__ void k_sum_parts(const double* __restrict__ part, int count, double* __restrict__ out) {
+  const double a = block_sum_array(part, count, 2, 0);
+  const double b = block_sum_array(part, count, 2, 1);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+__global__ void k_start_clock(Ctrl* c) { c->t0_ns = globaltimer_ns(); }
+
+}  // namespace numpmp_dev

@@ -1,0 +1,508 @@
+// pmp_kernels.cuh -- sm_100a kernels of the PMP/ADMM iteration.
+//
+// State layout (verified restatement of
+// solver.hpp:318-409).  The reference keeps the copies z in terminal space
+// (one per nonzero of R plus one per link).  Every reachable state has
+// z_t = A_j - B_l for the traffic terminal t = (l, j) and z_{s(l)} = zs_l
+// for the slack terminal, and the iteration preserves that form, so the
+// device keeps only stream-space (A, x) and link-space (B, zs, price, Q, v)
+// vectors:
+//
+//   v_l   = B_l + price_l / rho                        (written by K2)
+//   zeta_j = tau_j A_j - sum_{l in route(j)} v_l        (K1, route order)
+//   x_j   = prox(zeta_j)                  (prox.hpp:31-56, IEEE sqrt/div)
+//   A_j  <- alpha x_j + (1 - alpha) A_j
+//   ps_l  = max(zs_l - price_l/rho, -c_l)              (K2 epilogue)
+//   L_l   = sum_{j in link l} x_j    (ascending stream id, sequential)
+//   pbar_l = (L_l + ps_l) / (d_l + 1)   == compute_link_averages bit for bit
+//   B_l  <- alpha pbar_l + (1 - alpha) B_l
+//   zs_l <- alpha (ps_l - pbar_l) + (1 - alpha) zs_l
+//   price_l += rho (alpha pbar_l)
+//   r^2 = sum_l (d_l + 1) pbar_l^2
+//   s^2 = rho^2 [ sum_j tau_j dA_j^2 - 2 sum_l dB_l (R dA)_l
+//                 + sum_l d_l dB_l^2 + sum_l dzs_l^2 ]
+//
+// (R dA)_l is tracked without a second gather: Q_l = (R A)_l is kept as link
+// state, Q <- alpha L + (1 - alpha) Q, so (R dA)_l = Q_new - Q_old.  The
+// tracking error is damped by |1 - alpha| <= 1 every iteration.
+//
+// Kernels per iteration: K1 (stream pass over the CSC, R^T v gather + prox)
+// and K2 (link pass over the CSR, R x gather + link epilogue + residual
+// partials; its last block finalizes r, s, termination, trace and rho
+// balancing on the device, solver.hpp:450-476).  No host sync per iteration.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "numpmp_gpu.h"
+
+namespace numpmp_dev {
+
+constexpr int kWarps = 8;                 // warps per block (gather passes)
+constexpr int kThreads = kWarps * 32;
+constexpr int kChunk = 256;               // staged nonzeros per warp and round
+constexpr int kGroupsPerLane = kChunk / 128;  // int4 index groups per lane
+constexpr unsigned kFull = 0xffffffffu;
+
+enum : int { ST_RUNNING = -1, ST_CONVERGED = 0, ST_MAXITERS = 1, ST_TIMELIMIT = 2,
+             ST_NONFINITE = 3 };
+enum : int { MODE_RUN = 0, MODE_STEP = 1 };
+
+// Device-resident control block: the run loop of solver.hpp:450-476 lives
+// here, written only by the last block of the link pass.
+struct Ctrl {
+  double rho;        // rho for the next iteration
+  double rho_iter;   // rho used by the last completed iteration
+  double r_norm;
+  double s_norm;
+  long long iter;    // SolverState::iter
+  long long run_k;   // iteration counter of the current run (1-based)
+  long long trace_len;
+  long long t0_ns;   // %globaltimer at the start of the run
+  int done;          // 1: every later kernel of the batch exits at entry
+  int status;        // ST_*
+  int rho_changed;   // next K1 recomputes v = B + price / rho
+  unsigned ticket;   // last-block detection, link pass
+  unsigned ticket2;  // last-block detection, sharded gather pass
+  int pad;
+};
+
+struct IterArgs {
+  // stream side (CSC of R)
+  const int* col_ptr;      // n+1
+  const int* row_idx;      // nnz (+pad), link of each terminal in route order
+  const double* w;         // n
+  const unsigned char* kind;  // n
+  // link side (CSR of R, rows = links, ascending local stream ids)
+  const int* row_ptr;      // m+1
+  const int* col_idx;      // nnz (+pad)
+  const int* deg;          // m, global degree (sharded); null -> row_ptr diff
+  const double* cap;       // m
+  long long n, m;
+  // config
+  double alpha, eps_tol, mu, gamma;
+  long long rho_interval, trace_every, max_iters, time_limit_ns;
+  int mode;
+  // state, ping-pong: *_in is the current iterate, *_out the next
+  const double* A_in;
+  double* A_out;
+  double* x;
+  const double* B_in;
+  double* B_out;
+  const double* zs_in;
+  double* zs_out;
+  const double* pr_in;
+  double* pr_out;
+  const double* Q_in;
+  double* Q_out;
+  double* v;
+  double* k1_part;         // [grid1][2]: tau dA^2, objective
+  double* k2_part;         // [grid2][4]: r^2, dB.dQ, d dB^2, dzs^2
+  int grid1, grid2;
+  double* Lbuf;            // sharded: m partial loads + 2 scalars
+  Ctrl* ctrl;
+  numpmp_trace_row* trace;
+  long long trace_cap;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Streaming 128-bit index load: read once per pass, no L1 allocation, first
+// to be evicted from L2 so the gathered vectors stay resident.
+__device__ __forceinline__ int4 ld_stream_int4(const int* p, uint64_t pol) {
+  int4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_hint_f64(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ double dmax_ref(double a, double b) {  // std::max
+  return (a < b) ? b : a;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// prox.hpp:31-40 (two cancellation-safe branches, IEEE sqrt and division).
+__device__ __forceinline__ double prox_log(double z_sum, double w, double rho, int tau) {
+  const double t = static_cast<double>(tau);
+  const double d = 4.0 * w * t / rho;
+  const double root = sqrt(z_sum * z_sum + d);
+  if (z_sum >= 0.0) return (z_sum + root) / (2.0 * t);
+  return d / (2.0 * t * (root - z_sum));
+}
+// prox.hpp:44-56 (prox_linear_scalar clamped at zero, std::max semantics).
+__device__ __forceinline__ double prox_linear_nonneg(double z_sum, double w, double rho, int tau) {
+  const double x = (z_sum + w / rho) / static_cast<double>(tau);
+  return (x < 0.0) ? 0.0 : x;
+}
+
+struct GatherV {  // v_l (written by the previous link pass)
+  const double* __restrict__ v;
+  __device__ __forceinline__ double operator()(int l) const { return __ldg(v + l); }
+};
+struct GatherBU {  // v_l recomputed after a rho change / state upload
+  const double* __restrict__ B;
+  const double* __restrict__ pr;
+  double rho;
+  __device__ __forceinline__ double operator()(int l) const {
+    return __ldg(B + l) + __ldg(pr + l) / rho;
+  }
+};
+struct GatherX {  // x_j (written by this iteration's stream pass)
+  const double* __restrict__ x;
+  __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j); }
+};
+
+// Warp-cooperative segmented gather-sum.  The 32 lanes own contiguous,
+// lane-ordered segments [seg_beg, seg_end) tiling [span_beg, span_end) of
+// the index array.  The span is streamed with coalesced 128-bit index
+// loads, the gathered values are staged in shared memory, and each lane
+// then adds its own segment sequentially in index order -- the summation
+// order of the reference (route order for R^T v, ascending stream id for
+// R x), so link averages are bit-identical to compute_link_averages given
+// the same x.
+template <class G>
+__device__ __forceinline__ double warp_segmented_sum(const int* __restrict__ idx, int span_beg,
+                                                     int span_end, int seg_beg, int seg_end,
+                                                     double* __restrict__ sbuf, int lane, G g,
+                                                     uint64_t pol_stream) {
+  double acc = 0.0;
+  const int base0 = span_beg & ~3;
+  for (int cb = base0; cb < span_end; cb += kChunk) {
+    const int c0 = max(cb, span_beg);
+    const int c1 = min(cb + kChunk, span_end);
+    int4 iv[kGroupsPerLane];
+#pragma unroll
+    for (int i = 0; i < kGroupsPerLane; ++i) {
+      const int gpos = cb + 4 * (lane + 32 * i);
+      if (gpos < c1) iv[i] = ld_stream_int4(idx + gpos, pol_stream);
+    }
+    double vals[kGroupsPerLane][4];
+#pragma unroll
+    for (int i = 0; i < kGroupsPerLane; ++i) {
+      const int gpos = cb + 4 * (lane + 32 * i);
+      const int e[4] = {iv[i].x, iv[i].y, iv[i].z, iv[i].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pos = gpos + q;
+        vals[i][q] = (pos >= c0 && pos < c1) ? g(e[q]) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kGroupsPerLane; ++i) {
+      const int gpos = cb + 4 * (lane + 32 * i);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pos = gpos + q;
+        if (pos >= c0 && pos < c1) sbuf[pos - cb] = vals[i][q];
+      }
+    }
+    __syncwarp();
+    const int lo = max(seg_beg, c0), hi = min(seg_end, c1);
+    for (int k = lo; k < hi; ++k) acc += sbuf[k - cb];
+    __syncwarp();
+  }
+  return acc;
+}
+
+// Fixed-order block reduction of NV partials; thread 0 writes out[0..NV).
+template <int NV>
+__device__ __forceinline__ void block_sum_store(double (&v)[NV], double* out) {
+  __shared__ double red[kWarps][NV];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[wib][i] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s += red[w][i];
+      out[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Fixed-order sum of a strided partial array by one block; result on all threads.
+__device__ __forceinline__ double block_sum_array(const double* part, int count, int stride,
+                                                  int comp) {
+  __shared__ double red[kWarps];
+  __shared__ double total;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += __ldcg(part + i * stride + comp);
+  s = warp_sum(s);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (lane == 0) red[wib] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kWarps; ++w) t += red[w];
+    total = t;
+  }
+  __syncthreads();
+  const double r = total;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ bool kernel_should_exit(const Ctrl* ctrl) {
+  return *reinterpret_cast<const volatile int*>(&ctrl->done) != 0;
+}
+
+// ------------------------------------------------------------ K1: streams
+// R^T v gather over the CSC + prox + A update (solver.hpp:325-366 restated).
+template <class G>
+__device__ __forceinline__ void stream_pass_body(const IterArgs& a, G g, double rho, bool trace_it,
+                                                 double* sbuf, double& p_tda2, double& p_obj) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last();
+  const long long ntiles = (a.n + 31) / 32;
+  const double alpha = a.alpha;
+  for (long long tile = (long long)blockIdx.x * kWarps + wib; tile < ntiles;
+       tile += (long long)gridDim.x * kWarps) {
+    const long long j = tile * 32 + lane;
+    const bool valid = j < a.n;
+    const int beg = __ldg(a.col_ptr + (valid ? j : a.n));
+    const int end = valid ? __ldg(a.col_ptr + j + 1) : beg;
+    const int span_beg = __shfl_sync(kFull, beg, 0);
+    const int span_end = __shfl_sync(kFull, end, 31);
+    const double sum = warp_segmented_sum(a.row_idx, span_beg, span_end, beg, end, sbuf, lane, g,
+                                          pol_first);
+    if (valid) {
+      const int tau = end - beg;
+      const double A = ld_stream_f64(a.A_in + j, pol_first);
+      const double w = __ldg(a.w + j);
+      const int kd = __ldg(a.kind + j);
+      const double zeta = static_cast<double>(tau) * A - sum;
+      const double x = (kd == NUMPMP_KIND_LOG) ? prox_log(zeta, w, rho, tau)
+                                               : prox_linear_nonneg(zeta, w, rho, tau);
+      const double An = alpha * x + (1.0 - alpha) * A;
+      const double dA = An - A;
+      st_hint_f64(a.x + j, x, pol_last);
+      st_hint_f64(a.A_out + j, An, pol_first);
+      p_tda2 += static_cast<double>(tau) * dA * dA;
+      if (trace_it) p_obj += (kd == NUMPMP_KIND_LOG) ? w * log(x) : w * x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_stream_pass(IterArgs a) {
+  __shared__ double sbuf[kWarps][kChunk];
+  if (kernel_should_exit(a.ctrl)) return;
+  const double rho = a.ctrl->rho;
+  const bool rc = a.ctrl->rho_changed != 0;
+  const long long k = a.ctrl->run_k + 1;
+  const bool trace_it = (a.mode == MODE_RUN) && (k % a.trace_every == 0);
+  double part[2] = {0.0, 0.0};
+  double* sb = sbuf[threadIdx.x >> 5];
+  if (rc)
+    stream_pass_body(a, GatherBU{a.B_in, a.pr_in, rho}, rho, trace_it, sb, part[0], part[1]);
+  else
+    stream_pass_body(a, GatherV{a.v}, rho, trace_it, sb, part[0], part[1]);
+  block_sum_store<2>(part, a.k1_part + 2 * blockIdx.x);
+}
+
+// --------------------------------------------------------------- K2: links
+// Per-link epilogue: slack projection (solver.hpp:368-376), link average
+// (110-126), z update split into B / zs / Q (388-399), price (401-405).
+__device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, double L, int d,
+                                              double rho, double (&part)[4], uint64_t pol) {
+  const double alpha = a.alpha;
+  const double c = __ldg(a.cap + r);
+  const double pr = ld_stream_f64(a.pr_in + r, pol);
+  const double B = ld_stream_f64(a.B_in + r, pol);
+  const double zs = ld_stream_f64(a.zs_in + r, pol);
+  const double Q = ld_stream_f64(a.Q_in + r, pol);
+  const double u = pr / rho;
+  const double ps = dmax_ref(zs - u, -c);
+  const double cnt = static_cast<double>(d + 1);
+  const double pbar = (L + ps) / cnt;
+  part[0] += cnt * pbar * pbar;
+  const double Bn = alpha * pbar + (1.0 - alpha) * B;
+  const double dB = Bn - B;
+  const double zsn = alpha * (ps - pbar) + (1.0 - alpha) * zs;
+  const double dzs = zsn - zs;
+  const double Qn = alpha * L + (1.0 - alpha) * Q;
+  const double dQ = Qn - Q;
+  part[1] += dB * dQ;
+  part[2] += static_cast<double>(d) * dB * dB;
+  part[3] += dzs * dzs;
+  const double prn = pr + rho * (alpha * pbar);
+  a.B_out[r] = Bn;
+  a.zs_out[r] = zsn;
+  a.Q_out[r] = Qn;
+  a.pr_out[r] = prn;
+  a.v[r] = Bn + prn / rho;
+}
+
+// Finalize one iteration on the device: r, s, then the exact control order
+// of PmpSolver::run (solver.hpp:450-476).  Runs on one thread.
+__device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, double obj,
+                                   double r2, double cross, double ddb2, double dzs2) {
+  Ctrl* c = a.ctrl;
+  double s2r = tda2 - 2.0 * cross + ddb2 + dzs2;
+  if (s2r < 0.0) s2r = 0.0;  // rounding of the expanded form near zero
+  const double r_norm = sqrt(r2);
+  const double s_norm = sqrt(rho * rho * s2r);
+  c->iter += 1;
+  c->rho_iter = rho;
+  c->r_norm = r_norm;
+  c->s_norm = s_norm;
+  c->rho_changed = 0;
+  if (a.mode != MODE_RUN) return;  // step(): no control (solver.hpp:318-409)
+  const long long k = ++c->run_k;
+  if (!isfinite(r_norm) || !isfinite(s_norm)) {
+    c->status = ST_NONFINITE;
+    c->done = 1;
+    return;
+  }
+  if (r_norm < a.eps_tol && s_norm < a.eps_tol) {  // check_termination, strict
+    c->status = ST_CONVERGED;
+    c->done = 1;
+    return;
+  }
+  if (k % a.trace_every == 0 && c->trace_len < a.trace_cap) {
+    numpmp_trace_row row;
+    row.iter = k;
+    row.r_norm = r_norm;
+    row.s_norm = s_norm;
+    row.rho = rho;
+    row.objective = obj;
+    a.trace[c->trace_len++] = row;
+  }
+  if (a.time_limit_ns > 0 && globaltimer_ns() - c->t0_ns > a.time_limit_ns) {
+    c->status = ST_TIMELIMIT;
+    c->done = 1;
+    return;
+  }
+  if (k % a.rho_interval == 0) {  // update_rho (solver.hpp:168-174)
+    if (r_norm > a.mu * s_norm) {
+      c->rho = rho * a.gamma;
+      c->rho_changed = 1;
+    } else if (s_norm > a.mu * r_norm) {
+      c->rho = rho / a.gamma;
+      c->rho_changed = 1;
+    }
+  }
+  if (k >= a.max_iters) {
+    c->status = ST_MAXITERS;
+    c->done = 1;
+  }
+}
+
+enum : int { LP_FUSED = 0, LP_GATHER = 1, LP_EPILOGUE = 2 };
+
+// LP_FUSED: single GPU, gather + epilogue + finalize.
+// LP_GATHER: sharded, local partial loads -> Lbuf (+ K1 scalars), then NCCL.
+// LP_EPILOGUE: sharded, replicated epilogue on the all-reduced loads.
+template <int kPhase>
+__global__ void __launch_bounds__(kThreads) k_link_pass(IterArgs a) {
+  __shared__ double sbuf[kWarps][kChunk];
+  __shared__ bool s_last;
+  if (kernel_should_exit(a.ctrl)) return;
+  const double rho = a.ctrl->rho;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol_first = policy_evict_first();
+  const long long ngroups = (a.m + 31) / 32;
+  double part[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
+       g += (long long)gridDim.x * kWarps) {
+    const long long r = g * 32 + lane;
+    const bool valid = r < a.m;
+    double L;
+    int d;
+    if (kPhase == LP_EPILOGUE) {
+      if (!valid) continue;
+      L = __ldcg(a.Lbuf + r);
+      d = __ldg(a.deg + r);
+    } else {
+      const int rb = __ldg(a.row_ptr + (valid ? r : a.m));
+      const int re = valid ? __ldg(a.row_ptr + r + 1) : rb;
+      const int span_beg = __shfl_sync(kFull, rb, 0);
+      const int span_end = __shfl_sync(kFull, re, 31);
+      L = warp_segmented_sum(a.col_idx, span_beg, span_end, rb, re, sbuf[wib], lane,
+                             GatherX{a.x}, pol_first);
+      d = re - rb;
+      if (!valid) continue;
+      if (kPhase == LP_GATHER) {
+        a.Lbuf[r] = L;
+        continue;
+      }
+    }
+    link_epilogue(a, r, L, d, rho, part, pol_first);
+  }
+  if (kPhase == LP_GATHER) {
+    // The last block folds K1's scalar partials into Lbuf[m], Lbuf[m+1] so
+    // one all-reduce carries loads and scalars.
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket2, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double tda2 = block_sum_array(a.k1_part, a.grid1, 2, 0);
+    const double obj = block_sum_array(a.k1_part, a.grid1, 2, 1);
+    if (threadIdx.x == 0) {
+      a.Lbuf[a.m] = tda2;
+      a.Lbuf[a.m + 1] = obj;
+      a.ctrl->ticket2 = 0;
+    }
+    return;
+  }
+  block_sum_store<4>(part, a.k2_part + 4 * blockIdx.x);
+  __threadfence();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double tda2, obj;
+  if (kPhase == LP_EPILOGUE) {
+    tda2 = __ldcg(a.Lbuf + a.m);
+    obj = __ldcg(a.Lbuf + a.m + 1);
+  } else {
+    tda2 = block_sum_array(a.k1_part, a.grid1, 2, 0);
+    obj = block_sum_array(a.k1_part, a.grid1, 2, 1);
+  }
+  const double r2 = block_sum_array(a.k2_part, a.grid2, 4, 0);
+  const double cross = block_sum_array(a.k2_part, a.grid2, 4, 1);
+  const double ddb2 = block_sum_array(a.k2_part, a.grid2, 4, 2);
+  const double dzs2 = block_sum_array(a.k2_part, a.grid2, 4, 3);
+  if (threadIdx.x == 0) {
+    finalize_iteration(a, rho, tda2, obj, r2, cross, ddb2, dzs2);
+    a.ctrl->ticket = 0;
+    __threadfence();
+  }
+}
+
+}  // namespace numpmp_dev

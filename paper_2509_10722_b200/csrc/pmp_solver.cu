@@ -1,0 +1,1011 @@
+// pmp_solver.cu -- the C-ABI of libnumpmp_cuda.so (include/numpmp_gpu.h):
+// device problem, CSR build, state upload/materialisation and the
+// graph-batched, device-controlled PMP iteration loop.
+//
+// Reference boundary replaced: numpmp::PmpSolver (solver.hpp:265-519).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "numpmp_gpu.h"
+#include "numpmp_host.h"
+#include "pmp_aux.cuh"
+#include "pmp_kernels.cuh"
+
+using namespace numpmp_dev;
+
+namespace {
+
+constexpr int kBatchIters = 32;  // iterations per CUDA-graph launch (even)
+constexpr int kIdxPad = 64;      // int32 padding after index arrays (int4 over-read)
+
+struct GpuError {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      throw GpuError{NUMPMP_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+#define NK(call)                                                                           \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      throw GpuError{NUMPMP_NCCL_ERROR, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+thread_local std::string g_create_err;
+
+template <class T>
+T* dalloc(size_t count, int64_t* bytes) {
+  T* p = nullptr;
+  const size_t b = sizeof(T) * (count > 0 ? count : 1);
+  CK(cudaMalloc(&p, b));
+  *bytes += static_cast<int64_t>(b);
+  return p;
+}
+
+int grid_for(long long work, int threads = 256) {
+  long long b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 32) b = 148 * 32;
+  return static_cast<int>(b);
+}
+
+}  // namespace
+
+struct numpmp_gpu {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  numpmp_config cfg{};
+  int64_t m = 0, n = 0, nnz = 0;
+  int64_t n_total = 0, nnz_total = 0, stream_begin = 0;  // global sizes (sharded)
+  bool sharded = false;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int64_t dev_bytes = 0;
+
+  // problem
+  int* col_ptr = nullptr;
+  int* row_idx = nullptr;
+  double* w = nullptr;
+  unsigned char* kind = nullptr;
+  int* row_ptr = nullptr;
+  int* col_idx = nullptr;
+  int* deg = nullptr;  // global link degrees (sharded only)
+  double* cap = nullptr;
+
+  // state (ping-pong between iterations)
+  double* A[2] = {nullptr, nullptr};
+  double* B[2] = {nullptr, nullptr};
+  double* zs[2] = {nullptr, nullptr};
+  double* pr[2] = {nullptr, nullptr};
+  double* Q[2] = {nullptr, nullptr};
+  double* x = nullptr;
+  double* v = nullptr;
+  double* ps0 = nullptr;    // slack flows of an uploaded state
+  double* pbar0 = nullptr;  // link averages of an uploaded state
+  double* Lbuf = nullptr;   // m + 2
+  double* k1_part = nullptr;
+  double* k2_part = nullptr;
+  double* scratch_m = nullptr;
+  double* scratch_m2 = nullptr;
+  double* scratch_n = nullptr;
+  double* scalars = nullptr;  // 2
+  Ctrl* ctrl = nullptr;
+  Ctrl* ctrl_host = nullptr;  // pinned, 2 slots
+  numpmp_trace_row* trace_dev = nullptr;
+  int64_t trace_cap = 0;
+
+  int cur = 0;  // index of the current iterate buffers
+  int grid1 = 0, grid2 = 0;
+  int64_t iters_since_upload = 0;
+  bool host_p_valid = false;  // set_state keeps p / p_bar verbatim for get_state
+  std::vector<double> host_p, host_pbar;
+  int64_t run_iters = 0;
+  int last_status = NUMPMP_MAXITERS;
+
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t prof_graph[2] = {nullptr, nullptr};
+  cudaEvent_t ev_batch[2] = {nullptr, nullptr};
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_ev;  // 2 * kBatchIters + 1
+  int64_t prof_launches = 0, prof_iters = 0;
+  double prof_ms_k1 = 0.0, prof_ms_k2 = 0.0;
+
+  int64_t h2d = 0, d2h = 0;
+  cudaEvent_t ev_run[2] = {nullptr, nullptr};
+  double last_run_ms = 0.0;
+};
+
+namespace {
+
+int set_err(numpmp_gpu* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  g_create_err = msg;
+  return code;
+}
+
+const char* validate_config(const numpmp_config* c) {
+  // solver.hpp:32-44, same order and messages
+  if (!(c->eps_abs > 0.0)) return "eps_abs must be > 0";
+  if (!(c->rho0 > 0.0)) return "rho0 must be > 0";
+  if (!(c->alpha >= 1.0 && c->alpha <= 2.0)) return "alpha must be in [1, 2]";
+  if (!(c->mu > 1.0)) return "mu must be > 1";
+  if (!(c->gamma > 1.0)) return "gamma must be > 1";
+  if (c->rho_update_interval < 1) return "rho_update_interval must be >= 1";
+  if (c->max_iters < 1) return "max_iters must be >= 1";
+  if (c->trace_every < 1) return "trace_every must be >= 1";
+  if (c->threads < 0) return "threads must be >= 0";
+  if (c->time_limit < 0.0) return "time_limit must be >= 0";
+  return nullptr;
+}
+
+IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
+  IterArgs a{};
+  a.col_ptr = h->col_ptr;
+  a.row_idx = h->row_idx;
+  a.w = h->w;
+  a.kind = h->kind;
+  a.row_ptr = h->row_ptr;
+  a.col_idx = h->col_idx;
+  a.deg = h->deg;
+  a.cap = h->cap;
+  a.n = h->n;
+  a.m = h->m;
+  a.alpha = h->cfg.alpha;
+  // check_termination (solver.hpp:157-163): eps_abs * sqrt(J), J global.
+  a.eps_tol = h->cfg.eps_abs * std::sqrt(static_cast<double>(h->nnz_total + h->m));
+  a.mu = h->cfg.mu;
+  a.gamma = h->cfg.gamma;
+  a.rho_interval = h->cfg.rho_update_interval;
+  a.trace_every = h->cfg.trace_every;
+  a.max_iters = h->cfg.max_iters;
+  a.time_limit_ns = static_cast<long long>(h->cfg.time_limit * 1e9);
+  a.mode = mode;
+  const int i = parity, o = parity ^ 1;
+  a.A_in = h->A[i];
+  a.A_out = h->A[o];
+  a.x = h->x;
+  a.B_in = h->B[i];
+  a.B_out = h->B[o];
+  a.zs_in = h->zs[i];
+  a.zs_out = h->zs[o];
+  a.pr_in = h->pr[i];
+  a.pr_out = h->pr[o];
+  a.Q_in = h->Q[i];
+  a.Q_out = h->Q[o];
+  a.v = h->v;
+  a.k1_part = h->k1_part;
+  a.k2_part = h->k2_part;
+  a.grid1 = h->grid1;
+  a.grid2 = h->grid2;
+  a.Lbuf = h->Lbuf;
+  a.ctrl = h->ctrl;
+  a.trace = h->trace_dev;
+  a.trace_cap = h->trace_cap;
+  return a;
+}
+
+// One PMP iteration on the stream: K1, then K2 (fused) or K2a + NCCL
+// all-reduce of the partial link loads + K2b (sharded).  Optional events:
+// ev_start (before K1, may be null), ev_mid (after K1), ev_end (after K2).
+void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t ev_start,
+                       cudaEvent_t ev_mid, cudaEvent_t ev_end) {
+  IterArgs a = make_args(h, parity, mode);
+  if (ev_start) CK(cudaEventRecordWithFlags(ev_start, h->stream, cudaEventRecordExternal));
+  k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a);
+  CK(cudaGetLastError());
+  if (ev_mid) CK(cudaEventRecordWithFlags(ev_mid, h->stream, cudaEventRecordExternal));
+  if (!h->sharded) {
+    k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a);
+  } else {
+    k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+    NK(ncclAllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum,
+                     h->comm, h->stream));
+    k_link_pass<LP_EPILOGUE><<<h->grid2, kThreads, 0, h->stream>>>(a);
+  }
+  CK(cudaGetLastError());
+  if (ev_end) CK(cudaEventRecordWithFlags(ev_end, h->stream, cudaEventRecordExternal));
+}
+
+cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, bool with_events) {
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int i = 0; i < kBatchIters; ++i) {
+      cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+      if (with_events) {
+        e0 = i == 0 ? h->prof_ev[0] : nullptr;
+        e1 = h->prof_ev[static_cast<size_t>(2 * i + 1)];
+        e2 = h->prof_ev[static_cast<size_t>(2 * i + 2)];
+      }
+      enqueue_iteration(h, parity ^ (i & 1), MODE_RUN, e0, e1, e2);
+    }
+  } catch (...) {
+    cudaStreamEndCapture(h->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(h->stream, &g));
+  cudaGraphExec_t exec = nullptr;
+  CK(cudaGraphInstantiate(&exec, g, 0));
+  CK(cudaGraphDestroy(g));
+  return exec;
+}
+
+void upload(numpmp_gpu* h, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+  h->h2d += static_cast<int64_t>(bytes);
+}
+void download(numpmp_gpu* h, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+  h->d2h += static_cast<int64_t>(bytes);
+}
+
+Ctrl read_ctrl(numpmp_gpu* h) {
+  CK(cudaMemcpyAsync(h->ctrl_host, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return h->ctrl_host[0];
+}
+
+// Local per-link sums over this device's columns (+ NCCL sum when sharded).
+void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
+  k_row_sums<<<h->grid2, kThreads, 0, h->stream>>>(h->row_ptr, h->col_idx, src, h->m, out);
+  CK(cudaGetLastError());
+  if (h->sharded)
+    NK(ncclAllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm,
+                     h->stream));
+}
+
+// Link-major CSR of R on the device: a stable radix sort of the terminals
+// by link (stable => ascending terminal, hence ascending stream, within a
+// link, exactly the counting sort of model.hpp:193-199), then column index
+// = the terminal's stream.  sorted_terms_out (nullable, host) receives the
+// terminal ids in CSR order, i.e. the reference's link_terminals without
+// the slack terminals.
+void build_csr(numpmp_gpu* h, int* sorted_terms_out) {
+  const long long nnz = h->nnz;
+  int64_t tmpb = 0;
+  int* keys_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
+  int* vals_in = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
+  int* vals_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
+  int* t2s = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
+  void* temp = nullptr;
+  try {
+    k_iota<<<grid_for(nnz), 256, 0, h->stream>>>(vals_in, nnz);
+    k_terminal_stream<<<grid_for(h->n), 256, 0, h->stream>>>(h->col_ptr, h->n, t2s);
+    CK(cudaGetLastError());
+    int end_bit = 1;
+    while ((1ll << end_bit) < h->m) ++end_bit;
+    size_t temp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, h->row_idx, keys_out, vals_in,
+                                       vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
+    CK(cudaMalloc(&temp, temp_bytes > 0 ? temp_bytes : 1));
+    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, h->row_idx, keys_out, vals_in, vals_out,
+                                       static_cast<int>(nnz), 0, end_bit, h->stream));
+    k_row_ptr_from_sorted<<<grid_for(nnz + 1), 256, 0, h->stream>>>(keys_out, nnz, h->m,
+                                                                      h->row_ptr);
+    k_gather_i32<<<grid_for(nnz), 256, 0, h->stream>>>(t2s, vals_out, h->col_idx, nnz);
+    CK(cudaGetLastError());
+    if (sorted_terms_out)
+      download(h, sorted_terms_out, vals_out, sizeof(int) * static_cast<size_t>(nnz));
+    CK(cudaStreamSynchronize(h->stream));
+  } catch (...) {
+    cudaFree(temp);
+    cudaFree(keys_out);
+    cudaFree(vals_in);
+    cudaFree(vals_out);
+    cudaFree(t2s);
+    throw;
+  }
+  cudaFree(temp);
+  cudaFree(keys_out);
+  cudaFree(vals_in);
+  cudaFree(vals_out);
+  cudaFree(t2s);
+}
+
+void check_view(const numpmp_problem_view* pv) {
+  if (!pv || !pv->capacities || !pv->weights || !pv->kinds || !pv->stream_offsets ||
+      (pv->nnz > 0 && !pv->route_links))
+    throw GpuError{NUMPMP_INVALID_ARGUMENT, "problem view has null arrays"};
+  if (pv->m < 1 || pv->n < 1) throw GpuError{NUMPMP_VALIDATION_ERROR, "invalid problem: empty"};
+  if (pv->stream_offsets[0] != 0 || pv->stream_offsets[pv->n] != pv->nnz)
+    throw GpuError{NUMPMP_VALIDATION_ERROR,
+                   "invalid problem: [incidence-nnz: incidence nonzero count does not equal "
+                   "sum of route lengths]"};
+  if (pv->nnz >= (1LL << 31) - 2 * kIdxPad || pv->n >= (1LL << 31) - 1 ||
+      pv->m >= (1LL << 31) - 1)
+    throw GpuError{NUMPMP_INVALID_ARGUMENT, "problem exceeds the int32 index range of one device"};
+}
+
+void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  const int64_t m = h->m, n = h->n, nnz = h->nnz;
+  int64_t* b = &h->dev_bytes;
+  h->col_ptr = dalloc<int>(static_cast<size_t>(n) + 1, b);
+  h->row_idx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, b);
+  h->col_idx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, b);
+  h->row_ptr = dalloc<int>(static_cast<size_t>(m) + 1, b);
+  h->w = dalloc<double>(static_cast<size_t>(n), b);
+  h->kind = dalloc<unsigned char>(static_cast<size_t>(n), b);
+  h->cap = dalloc<double>(static_cast<size_t>(m), b);
+  for (int i = 0; i < 2; ++i) {
+    h->A[i] = dalloc<double>(static_cast<size_t>(n), b);
+    h->B[i] = dalloc<double>(static_cast<size_t>(m), b);
+    h->zs[i] = dalloc<double>(static_cast<size_t>(m), b);
+    h->pr[i] = dalloc<double>(static_cast<size_t>(m), b);
+    h->Q[i] = dalloc<double>(static_cast<size_t>(m), b);
+  }
+  h->x = dalloc<double>(static_cast<size_t>(n), b);
+  h->v = dalloc<double>(static_cast<size_t>(m), b);
+  h->ps0 = dalloc<double>(static_cast<size_t>(m), b);
+  h->pbar0 = dalloc<double>(static_cast<size_t>(m), b);
+  h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b);
+  h->scratch_m = dalloc<double>(static_cast<size_t>(m), b);
+  h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b);
+  h->scratch_n = dalloc<double>(static_cast<size_t>(n), b);
+  h->scalars = dalloc<double>(2, b);
+  h->ctrl = dalloc<Ctrl>(1, b);
+  CK(cudaMallocHost(&h->ctrl_host, 2 * sizeof(Ctrl)));
+  CK(cudaMemsetAsync(h->row_idx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
+  CK(cudaMemsetAsync(h->col_idx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
+  CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
+
+  // Upload.  Offsets travel as int64 and are narrowed on the device.
+  long long* off64 = nullptr;
+  CK(cudaMalloc(&off64, 8 * static_cast<size_t>(n + 1)));
+  upload(h, off64, pv->stream_offsets, 8 * static_cast<size_t>(n + 1));
+  k_offsets_to_i32<<<grid_for(n + 1), 256, 0, h->stream>>>(off64, h->col_ptr, n + 1);
+  CK(cudaGetLastError());
+  upload(h, h->row_idx, pv->route_links, 4 * static_cast<size_t>(nnz));
+  upload(h, h->w, pv->weights, 8 * static_cast<size_t>(n));
+  upload(h, h->kind, pv->kinds, static_cast<size_t>(n));
+  upload(h, h->cap, pv->capacities, 8 * static_cast<size_t>(m));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFree(off64);
+  build_csr(h, nullptr);
+
+  // Persistent grids: resident blocks x SMs.
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  int occ1 = 0, occ2 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
+  const long long tiles1 = (n + 31) / 32, tiles2 = (m + 31) / 32;
+  h->grid1 = static_cast<int>(std::max(
+      1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ1, 1))));
+  h->grid2 = static_cast<int>(std::max(
+      1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ2, 1))));
+  h->k1_part = dalloc<double>(2 * static_cast<size_t>(std::max(h->grid1, h->grid2)), b);
+  h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid2), b);
+  h->trace_cap = h->cfg.max_iters / h->cfg.trace_every + 2;
+  h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b);
+  for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&h->ev_batch[i], cudaEventDisableTiming));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+void reset_ctrl(numpmp_gpu* h, double rho, int64_t iter) {
+  Ctrl c{};
+  c.rho = rho;
+  c.rho_iter = rho;
+  c.iter = iter;
+  c.run_k = 0;
+  c.status = ST_RUNNING;
+  c.rho_changed = 1;  // the first K1 builds v from B and price
+  std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
+  CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+// Cold state (solver.hpp:293-303): p = z = 0, price = 0, rho = rho0.
+void do_set_cold(numpmp_gpu* h) {
+  h->cur = 0;
+  const size_t mb = 8 * static_cast<size_t>(h->m), nb = 8 * static_cast<size_t>(h->n);
+  CK(cudaMemsetAsync(h->A[0], 0, nb, h->stream));
+  CK(cudaMemsetAsync(h->x, 0, nb, h->stream));
+  CK(cudaMemsetAsync(h->B[0], 0, mb, h->stream));
+  CK(cudaMemsetAsync(h->zs[0], 0, mb, h->stream));
+  CK(cudaMemsetAsync(h->Q[0], 0, mb, h->stream));
+  CK(cudaMemsetAsync(h->pr[0], 0, mb, h->stream));
+  CK(cudaMemsetAsync(h->ps0, 0, mb, h->stream));
+  CK(cudaMemsetAsync(h->pbar0, 0, mb, h->stream));
+  h->host_p_valid = false;
+  h->iters_since_upload = 0;
+  reset_ctrl(h, h->cfg.rho0, 0);
+}
+
+// warm_state (solver.hpp:305-314) + warm_start_from (218-259).
+void do_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rho) {
+  if (!x0) throw GpuError{NUMPMP_INVALID_ARGUMENT, "warm start: x0 length does not match n"};
+  std::vector<uint8_t> kinds(static_cast<size_t>(h->n));
+  CK(cudaMemcpy(kinds.data(), h->kind, static_cast<size_t>(h->n), cudaMemcpyDeviceToHost));
+  for (int64_t j = 0; j < h->n; ++j)
+    if (kinds[static_cast<size_t>(j)] == NUMPMP_KIND_LOG && !(x0[j] > 0.0))
+      throw GpuError{NUMPMP_DOMAIN_ERROR, "warm start: log stream " +
+                                              std::to_string(j + h->stream_begin) +
+                                              " needs a positive rate"};
+  h->cur = 0;
+  const size_t nb = 8 * static_cast<size_t>(h->n), mb = 8 * static_cast<size_t>(h->m);
+  upload(h, h->x, x0, nb);
+  CK(cudaMemcpyAsync(h->A[0], h->x, nb, cudaMemcpyDeviceToDevice, h->stream));
+  global_row_sums(h, h->x, h->scratch_m);  // load = R x0, stream order per link
+  k_warm_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->deg, h->row_ptr, h->cap,
+                                                       h->m, h->B[0], h->zs[0], h->Q[0], h->ps0,
+                                                       h->pbar0);
+  CK(cudaGetLastError());
+  if (price)
+    upload(h, h->pr[0], price, mb);
+  else
+    CK(cudaMemsetAsync(h->pr[0], 0, mb, h->stream));
+  h->host_p_valid = false;
+  h->iters_since_upload = 0;
+  reset_ctrl(h, rho > 0.0 ? rho : h->cfg.rho0, 0);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+const char* numpmp_gpu_last_error(const numpmp_gpu* h) {
+  return h ? h->err.c_str() : g_create_err.c_str();
+}
+
+int numpmp_gpu_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(nullptr, NUMPMP_NCCL_ERROR, ncclGetErrorString(r));
+  std::memcpy(out128, &id, sizeof(id));
+  return NUMPMP_OK;
+}
+
+static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, int device,
+                       int rank, int world, const void* nccl_id, int64_t stream_begin,
+                       int64_t n_total, numpmp_gpu** out) {
+  if (!out) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (!cfg) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "config is null");
+  if (const char* msg = validate_config(cfg)) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, msg);
+  numpmp_gpu* h = nullptr;
+  try {
+    check_view(pv);
+    // model.hpp:76-155 on the host view (same rules and messages).
+    {
+      std::vector<char> msg(4096);
+      const int64_t nv = numpmp_validate(pv->m, pv->n, pv->capacities, pv->weights, pv->kinds,
+                                         pv->stream_offsets, pv->route_links, msg.data(),
+                                         static_cast<int64_t>(msg.size()));
+      if (nv > 0) throw GpuError{NUMPMP_VALIDATION_ERROR, msg.data()};
+    }
+    // solver.hpp:275-284: extension utilities have no device prox.
+    for (int64_t j = 0; j < pv->n; ++j)
+      if (pv->kinds[j] == NUMPMP_KIND_EXTENSION)
+        throw GpuError{NUMPMP_SOLVER_ERROR,
+                       "no extension registered for utility (extension utilities are host "
+                       "callbacks and are not supported by the device engine)"};
+    h = new numpmp_gpu();
+    h->cfg = *cfg;
+    h->device = device;
+    h->m = pv->m;
+    h->n = pv->n;
+    h->nnz = pv->nnz;
+    h->n_total = pv->n;
+    h->nnz_total = pv->nnz;
+    if (world > 1) {
+      h->sharded = true;
+      h->rank = rank;
+      h->world = world;
+      h->stream_begin = stream_begin;
+      h->n_total = n_total;
+      CK(cudaSetDevice(device));
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      NK(ncclCommInitRank(&h->comm, world, id, rank));
+    }
+    create_common(h, pv);
+    if (h->sharded) {
+      // Global link degrees and nnz: sums of the shards' local counts.
+      h->deg = dalloc<int>(static_cast<size_t>(h->m), &h->dev_bytes);
+      k_degree<<<grid_for(h->m), 256, 0, h->stream>>>(h->row_ptr, h->m, h->deg);
+      CK(cudaGetLastError());
+      NK(ncclAllReduce(h->deg, h->deg, static_cast<size_t>(h->m), ncclInt32, ncclSum, h->comm,
+                       h->stream));
+      double nnz_local = static_cast<double>(h->nnz);
+      CK(cudaMemcpyAsync(h->scalars, &nnz_local, 8, cudaMemcpyHostToDevice, h->stream));
+      NK(ncclAllReduce(h->scalars, h->scalars, 1, ncclDouble, ncclSum, h->comm, h->stream));
+      double nnz_global = 0.0;
+      CK(cudaMemcpyAsync(&nnz_global, h->scalars, 8, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      h->nnz_total = static_cast<int64_t>(nnz_global);
+    }
+    do_set_cold(h);
+    h->h2d = 0;
+    h->d2h = 0;
+    *out = h;
+    return NUMPMP_OK;
+  } catch (const GpuError& e) {
+    int code = e.code;
+    std::string msg = e.msg;
+    if (h) numpmp_gpu_destroy(h);
+    return set_err(nullptr, code, msg);
+  } catch (const std::bad_alloc&) {
+    if (h) numpmp_gpu_destroy(h);
+    return set_err(nullptr, NUMPMP_CUDA_ERROR, "host allocation failed");
+  }
+}
+
+int numpmp_gpu_create(const numpmp_problem_view* problem, const numpmp_config* config, int device,
+                      numpmp_gpu** out) {
+  return create_impl(problem, config, device, 0, 1, nullptr, 0, problem ? problem->n : 0, out);
+}
+
+int numpmp_gpu_create_sharded(const numpmp_problem_view* shard, const numpmp_config* config,
+                              int device, int rank, int world, const void* nccl_id,
+                              int64_t stream_begin, int64_t n_total, numpmp_gpu** out) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "bad rank/world");
+  if (world > 1 && !nccl_id) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "nccl_id is null");
+  return create_impl(shard, config, device, rank, world, nccl_id, stream_begin, n_total, out);
+}
+
+#define GUARD(h, ...)                                                   \
+  do {                                                                  \
+    if (!(h)) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle"); \
+    try {                                                               \
+      CK(cudaSetDevice((h)->device));                                   \
+      __VA_ARGS__;                                                      \
+      return NUMPMP_OK;                                                 \
+    } catch (const GpuError& e) {                                       \
+      return set_err((h), e.code, e.msg);                               \
+    } catch (const std::bad_alloc&) {                                   \
+      return set_err((h), NUMPMP_CUDA_ERROR, "host allocation failed"); \
+    }                                                                   \
+  } while (0)
+
+int numpmp_gpu_set_cold(numpmp_gpu* h) { GUARD(h, do_set_cold(h)); }
+
+int numpmp_gpu_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rho) {
+  GUARD(h, do_set_warm(h, x0, price, rho));
+}
+
+// Loads an arbitrary terminal-space state.  z is decomposed as
+// z_t = A_j - B_l by a breadth-first walk over each connected component of
+// the stream/link incidence (root link potential B = 0), then verified.
+int numpmp_gpu_set_state(numpmp_gpu* h, const double* p, const double* z, const double* p_bar,
+                         const double* price, double rho, int64_t iter) {
+  GUARD(h, {
+    if (h->sharded)
+      throw GpuError{NUMPMP_INVALID_ARGUMENT, "set_state is not supported on sharded handles"};
+    if (!p || !z || !p_bar || !price)
+      throw GpuError{NUMPMP_INVALID_ARGUMENT, "state arrays must not be null"};
+    if (!(rho > 0.0)) throw GpuError{NUMPMP_INVALID_ARGUMENT, "state rho must be > 0"};
+    const int64_t n = h->n, m = h->m, nnz = h->nnz;
+    std::vector<int> col_ptr(static_cast<size_t>(n) + 1), row_idx(static_cast<size_t>(nnz));
+    std::vector<int> row_ptr(static_cast<size_t>(m) + 1), col_idx(static_cast<size_t>(nnz));
+    CK(cudaMemcpy(col_ptr.data(), h->col_ptr, 4 * (n + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(row_idx.data(), h->row_idx, 4 * nnz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(row_ptr.data(), h->row_ptr, 4 * (m + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(col_idx.data(), h->col_idx, 4 * nnz, cudaMemcpyDeviceToHost));
+    // terminal of each CSR entry: position of link l in route j
+    std::vector<double> A(static_cast<size_t>(n), 0.0), Bv(static_cast<size_t>(m), 0.0);
+    std::vector<char> seen_s(static_cast<size_t>(n), 0), seen_l(static_cast<size_t>(m), 0);
+    std::vector<int64_t> queue;  // encoded: >= 0 link, < 0 stream (-(j+1))
+    auto term_of = [&](int64_t j, int l) -> int64_t {
+      for (int t = col_ptr[static_cast<size_t>(j)]; t < col_ptr[static_cast<size_t>(j) + 1]; ++t)
+        if (row_idx[static_cast<size_t>(t)] == l) return t;
+      return -1;
+    };
+    for (int64_t root = 0; root < m; ++root) {
+      if (seen_l[static_cast<size_t>(root)]) continue;
+      seen_l[static_cast<size_t>(root)] = 1;
+      Bv[static_cast<size_t>(root)] = 0.0;
+      queue.assign(1, root);
+      for (size_t qi = 0; qi < queue.size(); ++qi) {
+        const int64_t node = queue[qi];
+        if (node >= 0) {
+          const int l = static_cast<int>(node);
+          for (int k = row_ptr[static_cast<size_t>(l)]; k < row_ptr[static_cast<size_t>(l) + 1]; ++k) {
+            const int j = col_idx[static_cast<size_t>(k)];
+            if (seen_s[static_cast<size_t>(j)]) continue;
+            seen_s[static_cast<size_t>(j)] = 1;
+            A[static_cast<size_t>(j)] = z[term_of(j, l)] + Bv[static_cast<size_t>(l)];
+            queue.push_back(-(static_cast<int64_t>(j) + 1));
+          }
+        } else {
+          const int64_t j = -node - 1;
+          for (int t = col_ptr[static_cast<size_t>(j)]; t < col_ptr[static_cast<size_t>(j) + 1]; ++t) {
+            const int l = row_idx[static_cast<size_t>(t)];
+            if (seen_l[static_cast<size_t>(l)]) continue;
+            seen_l[static_cast<size_t>(l)] = 1;
+            Bv[static_cast<size_t>(l)] = A[static_cast<size_t>(j)] - z[t];
+            queue.push_back(l);
+          }
+        }
+      }
+    }
+    for (int64_t j = 0; j < n; ++j)
+      for (int t = col_ptr[static_cast<size_t>(j)]; t < col_ptr[static_cast<size_t>(j) + 1]; ++t) {
+        const double rec = A[static_cast<size_t>(j)] - Bv[static_cast<size_t>(row_idx[static_cast<size_t>(t)])];
+        const double scale = std::max({1.0, std::fabs(z[t]), std::fabs(A[static_cast<size_t>(j)])});
+        if (!(std::fabs(rec - z[t]) <= 1e-12 * scale))
+          throw GpuError{NUMPMP_INVALID_ARGUMENT,
+                         "state: z is not decomposable as A_j - B_l over the incidence"};
+      }
+    h->cur = 0;
+    const size_t nb = 8 * static_cast<size_t>(n), mb = 8 * static_cast<size_t>(m);
+    upload(h, h->A[0], A.data(), nb);
+    upload(h, h->B[0], Bv.data(), mb);
+    upload(h, h->zs[0], z + nnz, mb);
+    upload(h, h->pr[0], price, mb);
+    // stream rates of the given p (first terminal of each stream), for get_state
+    std::vector<double> x0(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) x0[static_cast<size_t>(j)] = p[col_ptr[static_cast<size_t>(j)]];
+    upload(h, h->x, x0.data(), nb);
+    global_row_sums(h, h->A[0], h->Q[0]);  // Q = R A
+    h->host_p.assign(p, p + nnz + m);
+    h->host_pbar.assign(p_bar, p_bar + m);
+    h->host_p_valid = true;
+    h->iters_since_upload = 0;
+    reset_ctrl(h, rho, iter);
+  });
+}
+
+int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, double* price,
+                         double* rho, int64_t* iter, double* prev_z) {
+  GUARD(h, {
+    const Ctrl c = read_ctrl(h);
+    const int64_t n = h->n, m = h->m, nnz = h->nnz;
+    const int cu = h->cur, pv = h->cur ^ 1;
+    const bool stepped = h->iters_since_upload > 0;
+    if (rho) *rho = c.rho;
+    if (iter) *iter = c.iter;
+    if (price) download(h, price, h->pr[cu], 8 * static_cast<size_t>(m));
+    double* ps_d = h->ps0;
+    double* pbar_d = h->pbar0;
+    if (stepped) {
+      // slack flows and averages of the last iteration, same arithmetic
+      global_row_sums(h, h->x, h->scratch_m);
+      k_materialize_links<<<grid_for(m), 256, 0, h->stream>>>(
+          h->scratch_m, h->deg, h->row_ptr, h->cap, h->zs[pv], h->pr[pv], c.rho_iter, m,
+          h->scratch_m2, h->Lbuf);
+      CK(cudaGetLastError());
+      ps_d = h->scratch_m2;
+      pbar_d = h->Lbuf;
+    }
+    const size_t J = static_cast<size_t>(nnz + m);
+    double *dp = nullptr, *dz = nullptr, *dzp = nullptr;
+    if (p || z || prev_z) {
+      if (p) CK(cudaMalloc(&dp, 8 * J));
+      if (z) CK(cudaMalloc(&dz, 8 * J));
+      if (prev_z) CK(cudaMalloc(&dzp, 8 * J));
+      k_expand_terminals<<<grid_for(n), 256, 0, h->stream>>>(
+          h->col_ptr, h->row_idx, n, h->x, h->A[cu], h->B[cu], h->A[pv], h->B[pv], dp, dz, dzp);
+      CK(cudaGetLastError());
+      if (dp) CK(cudaMemcpyAsync(dp + nnz, ps_d, 8 * m, cudaMemcpyDeviceToDevice, h->stream));
+      if (dz) CK(cudaMemcpyAsync(dz + nnz, h->zs[cu], 8 * m, cudaMemcpyDeviceToDevice, h->stream));
+      if (dzp) CK(cudaMemcpyAsync(dzp + nnz, h->zs[pv], 8 * m, cudaMemcpyDeviceToDevice, h->stream));
+      if (p) download(h, p, dp, 8 * J);
+      if (z) download(h, z, dz, 8 * J);
+      if (prev_z) download(h, prev_z, dzp, 8 * J);
+    }
+    if (p_bar) download(h, p_bar, pbar_d, 8 * static_cast<size_t>(m));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dp);
+    cudaFree(dz);
+    cudaFree(dzp);
+    if (!stepped && h->host_p_valid) {
+      if (p) std::memcpy(p, h->host_p.data(), 8 * J);
+      if (p_bar) std::memcpy(p_bar, h->host_pbar.data(), 8 * static_cast<size_t>(m));
+    }
+  });
+}
+
+int numpmp_gpu_step(numpmp_gpu* h, double* r_norm, double* s_norm) {
+  GUARD(h, {
+    enqueue_iteration(h, h->cur, MODE_STEP, nullptr, nullptr, nullptr);
+    const Ctrl c = read_ctrl(h);
+    h->cur ^= 1;
+    h->iters_since_upload += 1;
+    if (r_norm) *r_norm = c.r_norm;
+    if (s_norm) *s_norm = c.s_norm;
+  });
+}
+
+namespace {
+
+// The device-controlled loop of PmpSolver::run (solver.hpp:450-476).
+// Batches of kBatchIters iterations are launched as one CUDA graph; the
+// host looks at the control block of batch b only after batch b+1 is
+// queued, so the device never idles on the host.  Kernels queued after
+// the device set `done` exit at entry.
+void run_loop(numpmp_gpu* h) {
+  const int start = h->cur;
+  cudaGraphExec_t exec;
+  if (h->profiling) {
+    if (h->prof_ev.empty()) {
+      h->prof_ev.resize(2 * kBatchIters + 1);
+      for (auto& e : h->prof_ev) CK(cudaEventCreate(&e));
+    }
+    if (!h->prof_graph[start]) h->prof_graph[start] = build_graph(h, start, true);
+    exec = h->prof_graph[start];
+  } else {
+    if (!h->graph[start]) h->graph[start] = build_graph(h, start, false);
+    exec = h->graph[start];
+  }
+  // fresh run: control counters, trace, device clock
+  {
+    Ctrl c = read_ctrl(h);
+    c.run_k = 0;
+    c.trace_len = 0;
+    c.done = 0;
+    c.status = ST_RUNNING;
+    c.ticket = 0;
+    c.ticket2 = 0;
+    std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
+    CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  if (!h->ev_run[0]) {
+    CK(cudaEventCreate(&h->ev_run[0]));
+    CK(cudaEventCreate(&h->ev_run[1]));
+  }
+  CK(cudaEventRecord(h->ev_run[0], h->stream));
+  k_start_clock<<<1, 1, 0, h->stream>>>(h->ctrl);
+  CK(cudaGetLastError());
+  int64_t k_seen = 0;
+  int inflight = 0, slot = 0;
+  bool done = false;
+  while (!done) {
+    CK(cudaGraphLaunch(exec, h->stream));
+    CK(cudaMemcpyAsync(h->ctrl_host + slot, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaEventRecord(h->ev_batch[slot], h->stream));
+    ++inflight;
+    if (h->profiling) {
+      CK(cudaEventSynchronize(h->ev_batch[slot]));
+      const Ctrl& c = h->ctrl_host[slot];
+      const int64_t ran = c.run_k - k_seen;
+      for (int64_t i = 0; i < ran && i < kBatchIters; ++i) {
+        float t1 = 0.f, t2 = 0.f;
+        CK(cudaEventElapsedTime(&t1, h->prof_ev[static_cast<size_t>(2 * i)],
+                                h->prof_ev[static_cast<size_t>(2 * i + 1)]));
+        CK(cudaEventElapsedTime(&t2, h->prof_ev[static_cast<size_t>(2 * i + 1)],
+                                h->prof_ev[static_cast<size_t>(2 * i + 2)]));
+        h->prof_ms_k1 += t1;
+        h->prof_ms_k2 += t2;
+        h->prof_iters += 1;
+      }
+      k_seen = c.run_k;
+      done = c.done != 0;
+      inflight = 0;
+    } else if (inflight == 2) {
+      const int prev = slot ^ 1;
+      CK(cudaEventSynchronize(h->ev_batch[prev]));
+      done = h->ctrl_host[prev].done != 0;
+      --inflight;
+    }
+    slot ^= 1;
+    h->prof_launches += kBatchIters * (h->sharded ? 3 : 2);
+  }
+  CK(cudaEventRecord(h->ev_run[1], h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const Ctrl c = read_ctrl(h);
+  {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev_run[0], h->ev_run[1]));
+    h->last_run_ms = ms;
+  }
+  h->run_iters = c.run_k;
+  h->iters_since_upload += c.run_k;
+  h->cur = static_cast<int>((start + c.run_k) & 1);
+  if (c.status == ST_NONFINITE)
+    throw GpuError{NUMPMP_SOLVER_ERROR,
+                   "non-finite state at iteration " + std::to_string(c.run_k)};
+  h->last_status = c.status == ST_CONVERGED ? NUMPMP_CONVERGED
+                   : c.status == ST_TIMELIMIT ? NUMPMP_TIMELIMIT
+                                              : NUMPMP_MAXITERS;
+}
+
+// Solution post-processing (solver.hpp:478-504) on the device.
+void post_process(numpmp_gpu* h, double* x, double* s, double* lambda, double* lambda_raw,
+                  numpmp_solution_info* info, numpmp_trace_row* trace, int64_t trace_cap) {
+  const Ctrl c = read_ctrl(h);
+  const int cu = h->cur;
+  const int gpost = std::min(grid_for(h->n), h->grid1);
+  k_post_streams<<<gpost, kThreads, 0, h->stream>>>(h->x, h->w, h->kind, h->n, h->cfg.eps_abs,
+                                                   h->scratch_n, h->k1_part);
+  CK(cudaGetLastError());
+  k_sum_parts<<<1, kThreads, 0, h->stream>>>(h->k1_part, gpost, h->scalars);
+  CK(cudaGetLastError());
+  if (h->sharded)
+    NK(ncclAllReduce(h->scalars, h->scalars, 2, ncclDouble, ncclSum, h->comm, h->stream));
+  global_row_sums(h, h->scratch_n, h->scratch_m);  // load = R x (clamped x)
+  k_post_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->cap, h->pr[cu], h->m,
+                                                      h->scratch_m2, h->Lbuf);
+  CK(cudaGetLastError());
+  double obj[2] = {0.0, 0.0};
+  CK(cudaMemcpyAsync(obj, h->scalars, 16, cudaMemcpyDeviceToHost, h->stream));
+  if (x) download(h, x, h->scratch_n, 8 * static_cast<size_t>(h->n));
+  if (s) download(h, s, h->scratch_m2, 8 * static_cast<size_t>(h->m));
+  if (lambda) download(h, lambda, h->Lbuf, 8 * static_cast<size_t>(h->m));
+  if (lambda_raw) download(h, lambda_raw, h->pr[cu], 8 * static_cast<size_t>(h->m));
+  int64_t tl = std::min<int64_t>(c.trace_len, h->trace_cap);
+  std::vector<numpmp_trace_row> rows(static_cast<size_t>(tl) + 1);
+  if (tl > 0) download(h, rows.data(), h->trace_dev, sizeof(numpmp_trace_row) * tl);
+  CK(cudaStreamSynchronize(h->stream));
+  // Final trace sample (solver.hpp:478-481).
+  if (tl == 0 || rows[static_cast<size_t>(tl) - 1].iter != c.iter) {
+    numpmp_trace_row& r = rows[static_cast<size_t>(tl)];
+    r.iter = c.iter;
+    r.r_norm = c.r_norm;
+    r.s_norm = c.s_norm;
+    r.rho = c.rho;
+    r.objective = obj[1];
+    ++tl;
+  }
+  if (trace)
+    std::memcpy(trace, rows.data(), sizeof(numpmp_trace_row) * static_cast<size_t>(std::min(tl, trace_cap)));
+  if (info) {
+    info->objective = obj[0];
+    info->r_norm = c.r_norm;
+    info->s_norm = c.s_norm;
+    info->rho_final = c.rho;
+    info->iterations = c.iter;
+    info->status = h->last_status;
+    info->trace_len = tl;
+  }
+}
+
+}  // namespace
+
+int numpmp_gpu_run(numpmp_gpu* h, double* x, double* s, double* lambda, double* lambda_raw,
+                   numpmp_solution_info* info, numpmp_trace_row* trace, int64_t trace_cap) {
+  GUARD(h, {
+    run_loop(h);
+    post_process(h, x, s, lambda, lambda_raw, info, trace, trace_cap);
+  });
+}
+
+int numpmp_gpu_run_device(numpmp_gpu* h, numpmp_solution_info* info) {
+  GUARD(h, {
+    run_loop(h);
+    const Ctrl c = read_ctrl(h);
+    if (info) {
+      std::memset(info, 0, sizeof(*info));
+      info->r_norm = c.r_norm;
+      info->s_norm = c.s_norm;
+      info->rho_final = c.rho;
+      info->iterations = c.iter;
+      info->status = h->last_status;
+      info->trace_len = c.trace_len;
+    }
+  });
+}
+
+int numpmp_gpu_export_layout(numpmp_gpu* h, int64_t* link_offsets, int64_t* link_terminals,
+                             int32_t* link_counts) {
+  GUARD(h, {
+    if (h->sharded)
+      throw GpuError{NUMPMP_INVALID_ARGUMENT, "export_layout is not supported on sharded handles"};
+    const int64_t m = h->m, nnz = h->nnz;
+    std::vector<int> row_ptr(static_cast<size_t>(m) + 1), terms(static_cast<size_t>(nnz));
+    // Rebuild the sort to recover the terminal ids; the device CSR itself
+    // is checked against them (column = stream of terminal).
+    build_csr(h, terms.data());
+    CK(cudaMemcpy(row_ptr.data(), h->row_ptr, 4 * (m + 1), cudaMemcpyDeviceToHost));
+    // model.hpp:182-199: |l| = degree + 1, slack terminal nnz + l last.
+    link_offsets[0] = 0;
+    for (int64_t l = 0; l < m; ++l) {
+      const int64_t d = row_ptr[static_cast<size_t>(l) + 1] - row_ptr[static_cast<size_t>(l)];
+      if (link_counts) link_counts[l] = static_cast<int32_t>(d + 1);
+      link_offsets[l + 1] = link_offsets[l] + d + 1;
+      int64_t o = link_offsets[l];
+      for (int k = row_ptr[static_cast<size_t>(l)]; k < row_ptr[static_cast<size_t>(l) + 1]; ++k)
+        link_terminals[o++] = terms[static_cast<size_t>(k)];
+      link_terminals[o] = nnz + l;
+    }
+  });
+}
+
+int numpmp_gpu_sizes(const numpmp_gpu* h, int64_t* m, int64_t* n, int64_t* nnz) {
+  if (!h) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle");
+  if (m) *m = h->m;
+  if (n) *n = h->n;
+  if (nnz) *nnz = h->nnz;
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_set_profiling(numpmp_gpu* h, int enable) {
+  if (!h) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle");
+  h->profiling = enable != 0;
+  h->prof_launches = 0;
+  h->prof_iters = 0;
+  h->prof_ms_k1 = 0.0;
+  h->prof_ms_k2 = 0.0;
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_profile(const numpmp_gpu* h, int64_t* launches, double* ms_stream_pass,
+                       double* ms_link_pass, int64_t* iterations_timed) {
+  if (!h) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle");
+  if (launches) *launches = h->prof_launches;
+  if (ms_stream_pass) *ms_stream_pass = h->prof_ms_k1;
+  if (ms_link_pass) *ms_link_pass = h->prof_ms_k2;
+  if (iterations_timed) *iterations_timed = h->prof_iters;
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_last_run_ms(const numpmp_gpu* h, double* ms) {
+  if (!h) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle");
+  if (ms) *ms = h->last_run_ms;
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_pin_host(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return NUMPMP_OK;
+  cudaError_t e = cudaHostRegister(ptr, static_cast<size_t>(bytes), cudaHostRegisterDefault);
+  if (e != cudaSuccess) return set_err(nullptr, NUMPMP_CUDA_ERROR, cudaGetErrorString(e));
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_unpin_host(void* ptr) {
+  if (!ptr) return NUMPMP_OK;
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) return set_err(nullptr, NUMPMP_CUDA_ERROR, cudaGetErrorString(e));
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_transfer_bytes(const numpmp_gpu* h, int64_t* h2d, int64_t* d2h) {
+  if (!h) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle");
+  if (h2d) *h2d = h->h2d;
+  if (d2h) *d2h = h->d2h;
+  return NUMPMP_OK;
+}
+
+void numpmp_gpu_destroy(numpmp_gpu* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (int i = 0; i < 2; ++i) {
+    if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
+    if (h->prof_graph[i]) cudaGraphExecDestroy(h->prof_graph[i]);
+    if (h->ev_batch[i]) cudaEventDestroy(h->ev_batch[i]);
+    cudaFree(h->A[i]);
+    cudaFree(h->B[i]);
+    cudaFree(h->zs[i]);
+    cudaFree(h->pr[i]);
+    cudaFree(h->Q[i]);
+  }
+  for (auto& e : h->prof_ev) cudaEventDestroy(e);
+  for (auto& e : h->ev_run)
+    if (e) cudaEventDestroy(e);
+  void* bufs[] = {h->col_ptr, h->row_idx, h->w,        h->kind,     h->row_ptr,   h->col_idx,
+                  h->deg,     h->cap,     h->x,        h->v,        h->ps0,       h->pbar0,
+                  h->Lbuf,    h->k1_part, h->k2_part,  h->scratch_m, h->scratch_m2, h->scratch_n,
+                  h->scalars, h->ctrl,    h->trace_dev};
+  for (void* p : bufs) cudaFree(p);
+  if (h->ctrl_host) cudaFreeHost(h->ctrl_host);
+  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

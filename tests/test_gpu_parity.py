@@ -1,0 +1,416 @@
+"""GPU parity tests: the sm_100a engine (through the C-ABI, via the Python
+mirror of the reference API) against the CPU oracle and the reference's own
+golden vectors.
+
+Tolerance (fp64): 1e-6 relative, measured in the max norm of each compared
+vector (|a - b|_inf <= 1e-6 * max(|b|_inf, floor)); iteration counts must
+be equal; the layout must be bit-exact.  The golden values of
+proj/tests/test_solver.cpp are asserted at the tolerances that file uses.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pmp = pytest.importorskip("paper_2509_10722_b200")
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-6
+
+
+def close(a, b, rtol=RTOL, floor=1e-12):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    scale = max(float(np.max(np.abs(b))) if b.size else 0.0, floor)
+    err = float(np.max(np.abs(a - b))) if b.size else 0.0
+    return err <= rtol * scale, err / scale
+
+
+def bipartite_fixture():
+    # test_solver.cpp:15-20
+    S = pmp.Stream
+    return pmp.build_problem([S(0, pmp.StreamKind.Log, "", 1.0, [0]),
+                              S(1, pmp.StreamKind.Log, "", 1.0, [1, 2]),
+                              S(2, pmp.StreamKind.Log, "", 1.0, [1])], [1.0, 1.0, 1.0])
+
+
+def single(kind=pmp.StreamKind.Log, w=1.0, route=(0,), caps=(1.0,)):
+    return pmp.build_problem([pmp.Stream(0, kind, "", w, list(route))], list(caps))
+
+
+def plain_config(rho0):
+    return pmp.SolverConfig(alpha=1.0, rho0=rho0, rho_update_interval=1000000)
+
+
+def ocfg(o, c: "pmp.SolverConfig"):
+    return o.Config(eps_abs=c.eps_abs, rho0=c.rho0, alpha=c.alpha, mu=c.mu, gamma=c.gamma,
+                    time_limit=c.time_limit, rho_update_interval=c.rho_update_interval,
+                    max_iters=c.max_iters, trace_every=c.trace_every)
+
+
+# ---------------------------------------------------- golden vectors (reference tests)
+def test_first_iteration_from_zero_state():
+    # test_solver.cpp:110-124
+    p = single()
+    with pmp.PmpSolver(p, plain_config(1.0)) as s:
+        st = s.cold_state()
+        s.step(st)
+    assert st.iter == 1
+    np.testing.assert_allclose(st.p, [1.0, 0.0], rtol=0, atol=4e-16)
+    np.testing.assert_allclose(st.p_bar, [0.5], rtol=0, atol=4e-16)
+    np.testing.assert_allclose(st.z, [0.5, -0.5], rtol=0, atol=4e-16)
+    np.testing.assert_allclose(st.price, [0.5], rtol=0, atol=4e-16)
+
+
+@pytest.mark.parametrize("rho0", [1.0, 2.0])
+def test_alpha1_matches_plain_transcription(rho0, restatement, oracle_mod):
+    # test_solver.cpp:126-146 / acceptance.cpp criterion 7
+    p = bipartite_fixture()
+    a = oracle_mod.arrays_from(p)
+    J = a.J
+    pp, uu, pbar, arg = np.zeros(J), np.zeros(J), np.zeros(p.m), np.zeros(J)
+    pr, keep = restatement._prob(a)
+    with pmp.PmpSolver(p, plain_config(rho0)) as s:
+        st = s.cold_state()
+        for it in range(100):
+            s.step(st)
+            restatement.L.oracle_plain_step(
+                __import__("ctypes").byref(pr), __import__("ctypes").c_double(rho0),
+                *[oracle_mod._p(v) for v in (pp, uu, pbar, arg)])
+            ok, err = close(st.p, pp, 1e-12)
+            assert ok, (it, err)
+            price_ref = rho0 * uu[: J]
+            ok, err = close(st.price[a.terminal_link], price_ref, 1e-12)
+            assert ok, (it, err)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 1.6])
+def test_fixed_point_is_stationary(alpha):
+    # test_solver.cpp:148-171
+    p = single()
+    cfg = pmp.SolverConfig(alpha=alpha, rho_update_interval=1000000)
+    with pmp.PmpSolver(p, cfg) as s:
+        st = s.cold_state()
+        st.p = np.array([1.0, -1.0])
+        st.z = np.array([1.0, -1.0])
+        st.p_bar = np.array([0.0])
+        st.price = np.array([1.0])
+        r, sn = s.step(st)
+    np.testing.assert_allclose(st.p, [1.0, -1.0], atol=1e-14)
+    np.testing.assert_allclose(st.z, [1.0, -1.0], atol=1e-14)
+    np.testing.assert_allclose(st.price, [1.0], atol=1e-14)
+    assert abs(r) <= 1e-14 and abs(sn) <= 1e-14
+
+
+def test_single_log_stream_analytic():
+    # test_solver.cpp:75-84
+    with pmp.PmpSolver(single(), pmp.SolverConfig(eps_abs=1e-8)) as s:
+        sol = s.solve()
+    assert sol.status == pmp.SolveStatus.Converged
+    assert abs(sol.x[0] - 1.0) <= 1e-6
+    assert abs(sol.lambda_[0] - 1.0) <= 1e-6
+
+
+def test_single_linear_stream_saturates():
+    # test_solver.cpp:86-96
+    with pmp.PmpSolver(single(pmp.StreamKind.Linear, caps=(5.0,)), pmp.SolverConfig(eps_abs=1e-8)) as s:
+        sol = s.solve()
+    assert sol.status == pmp.SolveStatus.Converged
+    assert abs(sol.x[0] - 5.0) <= 1e-5
+    assert abs(sol.objective - 5.0) <= 1e-5
+
+
+def test_bipartite_fixture_solution():
+    # test_solver.cpp:98-108 + test_oracle.cpp:63-76: x = (1, .5, .5), lambda = (1, 2, 0)
+    with pmp.PmpSolver(bipartite_fixture(), pmp.SolverConfig(eps_abs=1e-7)) as s:
+        sol = s.solve()
+    assert sol.status == pmp.SolveStatus.Converged
+    for got, want in zip(sol.x, [1.0, 0.5, 0.5]):
+        assert abs(got - want) <= 1e-4 * want
+    np.testing.assert_allclose(sol.lambda_, [1.0, 2.0, 0.0], atol=1e-3)
+
+
+def test_non_binding_link_dual_vanishes():
+    # test_solver.cpp:370-382
+    p = single(route=(0, 1), caps=(1.0, 5.0))
+    with pmp.PmpSolver(p, pmp.SolverConfig(eps_abs=1e-8)) as s:
+        sol = s.solve()
+    assert sol.status == pmp.SolveStatus.Converged
+    assert abs(sol.x[0] - 1.0) <= 1e-5
+    assert abs(sol.lambda_[0] - 1.0) <= 1e-3
+    assert abs(sol.lambda_[1]) <= 1e-3
+
+
+def test_max_iters_status_is_returned_not_thrown():
+    # test_solver.cpp:384-393
+    with pmp.PmpSolver(bipartite_fixture(), pmp.SolverConfig(max_iters=3, eps_abs=1e-12)) as s:
+        sol = s.solve()
+    assert sol.status == pmp.SolveStatus.MaxIters
+    assert sol.iterations == 3
+
+
+def test_non_finite_state_reports_iteration_number():
+    # test_solver.cpp:173-186
+    p = single(w=1e308)
+    with pmp.PmpSolver(p, pmp.SolverConfig(rho0=1e-8)) as s:
+        with pytest.raises(pmp.SolverError, match="iteration 1"):
+            s.solve()
+
+
+def test_trace_contract():
+    # test_solver.cpp:395-415
+    p = pmp.gen_uncongested(pmp.GenSpec(m=60, n=30, seed=4))
+    with pmp.PmpSolver(p, pmp.SolverConfig(eps_abs=1e-6, trace_every=10)) as s:
+        sol = s.solve()
+    assert sol.trace
+    its = [t.iter for t in sol.trace]
+    assert all(a < b for a, b in zip(its, its[1:]))
+    assert sol.trace[-1].iter == sol.iterations
+    assert sol.trace[-1].r_norm == sol.r_norm and sol.trace[-1].s_norm == sol.s_norm
+    assert all(t.iter % 10 == 0 for t in sol.trace[:-1])
+
+
+def test_warm_start_from_optimum_converges_immediately():
+    # test_solver.cpp:322-339
+    p = pmp.gen_uncongested(pmp.GenSpec(m=80, n=40, avg_links_per_stream=4.0, seed=21))
+    with pmp.PmpSolver(p, pmp.SolverConfig(eps_abs=1e-7)) as s:
+        cold = s.solve()
+        assert cold.status == pmp.SolveStatus.Converged
+        rerun = s.solve(pmp.WarmStart(cold.x, cold.lambda_raw, cold.rho_final))
+    assert rerun.status == pmp.SolveStatus.Converged
+    assert rerun.iterations <= 5
+
+
+def test_warm_start_validation():
+    # test_solver.cpp:341-350
+    with pmp.PmpSolver(bipartite_fixture(), pmp.SolverConfig()) as s:
+        with pytest.raises(ValueError):
+            s.warm_state(pmp.WarmStart(np.array([1.0, 1.0])))
+        with pytest.raises(pmp.DomainError):
+            s.warm_state(pmp.WarmStart(np.array([1.0, 0.0, 1.0])))
+        with pytest.raises(ValueError):
+            s.warm_state(pmp.WarmStart(np.array([1.0, 1.0, 1.0]), np.array([0.1])))
+
+
+def test_warm_start_slack_flows():
+    # test_solver.cpp:352-368
+    p = bipartite_fixture()
+    with pmp.PmpSolver(p, pmp.SolverConfig()) as s:
+        st = s.warm_state(pmp.WarmStart(np.array([0.25, 0.5, 0.75]), None, 1.0))
+    nnz = p.nnz
+    np.testing.assert_array_equal(st.p[nnz:], [-0.25, -1.0, -0.5])
+    tl = p.layout.terminal_link
+    np.testing.assert_array_equal(st.z, st.p - st.p_bar[tl])
+
+
+# ------------------------------------------------------------ oracle parity
+def _gen(m, n, avg, kind, uniform, seed):
+    w = pmp.WeightDist.uniform(0.5, 1.5) if uniform else pmp.WeightDist.constant(1.0)
+    return pmp.gen_uncongested(pmp.GenSpec(m=m, n=n, avg_links_per_stream=avg, kind=pmp.GenKind(kind),
+                                           weights=w, seed=seed))
+
+
+SOLVE_CASES = [
+    # (m, n, avg, kind, uniform weights, seed, eps, rho0)
+    (1000, 10000, 5.0, 0, False, 7, 1e-4, 1.0),      # config A, library default rho0
+    (1000, 10000, 5.0, 0, False, 7, 1e-4, 1000.0),   # config A, large-instance rho0
+    (300, 150, 4.0, 2, True, 3, 1e-6, 1.0),          # mixed log/linear
+    (2000, 4000, 6.0, 2, True, 11, 1e-5, 1000.0),    # mixed, rho balancing active
+    (100, 50, 5.0, 2, True, 1, 1e-6, 1.0),           # ConvergedRunsAreFeasible instance
+]
+
+
+@pytest.mark.parametrize("case", SOLVE_CASES)
+def test_solve_matches_oracle(case, restatement, oracle_mod):
+    m, n, avg, kind, uni, seed, eps, rho0 = case
+    p = _gen(m, n, avg, kind, uni, seed)
+    cfg = pmp.SolverConfig(eps_abs=eps, rho0=rho0)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+        fin = s.final_state()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert ref.error is None
+    assert sol.iterations == ref.iterations
+    assert int(sol.status) == ref.status
+    assert sol.rho_final == ref.rho_final
+    for name, got, want in [("x", sol.x, ref.x), ("lambda_raw", sol.lambda_raw, ref.lambda_raw),
+                            ("s", sol.s, ref.s), ("lambda", sol.lambda_, ref.lambda_)]:
+        ok, err = close(got, want)
+        assert ok, (name, err)
+    assert abs(sol.objective - ref.objective) <= RTOL * abs(ref.objective)
+    assert len(sol.trace) == ref.trace.shape[0]
+    for row, want in zip(sol.trace, ref.trace):
+        assert row.iter == int(want[0]) and row.rho == want[3]
+        for got, w in [(row.r_norm, want[1]), (row.s_norm, want[2]), (row.objective, want[4])]:
+            assert abs(got - w) <= RTOL * abs(w) + 1e-300, (row.iter, got, w)
+    ok, err = close(fin.z, ref.final_z)
+    assert ok, err
+    ok, err = close(fin.p, ref.final_p)
+    assert ok, err
+
+
+@pytest.mark.parametrize("K", [1, 10, 100])
+def test_step_state_matches_oracle(K, restatement, oracle_mod):
+    # state-level parity of step() on config A
+    p = _gen(1000, 10000, 5.0, 0, False, 7)
+    cfg = pmp.SolverConfig(rho0=1.0)
+    a = oracle_mod.arrays_from(p)
+    oc = ocfg(oracle_mod, cfg)
+    ost = restatement.cold_state(a, oc)
+    with pmp.PmpSolver(p, cfg) as s:
+        st = s.cold_state()
+        for _ in range(K):
+            r, sn = s.step(st)
+            ro, so, _ = restatement.step(a, oc, ost)
+            assert abs(r - ro) <= RTOL * ro and abs(sn - so) <= RTOL * so
+    for key in ("p", "z", "p_bar", "price"):
+        ok, err = close(getattr(st, key), ost[key])
+        assert ok, (key, err)
+    assert st.iter == ost["iter"] == K
+
+
+def test_warm_solve_matches_oracle(restatement, oracle_mod):
+    # degrade workflow (config D shape, small): warm start from a prior solve
+    base = _gen(500, 2000, 6.0, 2, True, 17)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1.0)
+    with pmp.PmpSolver(base, cfg) as s:
+        prior = s.solve()
+    deg = pmp.degrade(base, 0.5, 0.5, 99)
+    ratio = deg.capacities / base.capacities
+    x0 = prior.x.copy()
+    for j in range(deg.n):
+        x0[j] *= min(1.0, float(np.min(ratio[deg.route(j)])))
+        if deg.kinds[j] == 0 and not x0[j] > 0:
+            x0[j] = 1e-8
+    warm = pmp.WarmStart(x0, prior.lambda_raw / ratio, prior.rho_final / float(ratio.min()))
+    with pmp.PmpSolver(deg, cfg) as s:
+        sol = s.solve(warm)
+    ref = restatement.solve(oracle_mod.arrays_from(deg), ocfg(oracle_mod, cfg), (warm.x0, warm.price, warm.rho))
+    assert sol.iterations == ref.iterations
+    ok, err = close(sol.x, ref.x)
+    assert ok, err
+    ok, err = close(sol.lambda_raw, ref.lambda_raw)
+    assert ok, err
+
+
+def test_termination_contract_post_hoc(restatement, oracle_mod):
+    # acceptance.cpp criterion 4: residuals recomputed from the final state
+    p = _gen(100, 50, 5.0, 2, True, 2)
+    cfg = pmp.SolverConfig(eps_abs=1e-6)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+        st = s.final_state()
+        prev_z = s.final_prev_z()
+    a = oracle_mod.arrays_from(p)
+    pbar = np.empty(p.m)
+    pr, keep = restatement._prob(a)
+    import ctypes
+
+    restatement.L.oracle_link_averages(ctypes.byref(pr), oracle_mod._p(st.p), oracle_mod._p(pbar))
+    r = math.sqrt(float(np.sum(a.link_counts * pbar * pbar)))
+    sn = math.sqrt(float(np.sum((st.rho * (st.z - prev_z)) ** 2)))
+    eps_tol = 1e-6 * math.sqrt(a.J)
+    assert r < eps_tol and sn < eps_tol
+    assert abs(r - sol.r_norm) <= 1e-9 * eps_tol and abs(sn - sol.s_norm) <= 1e-6 * eps_tol
+
+
+def test_layout_bit_exact_with_reference(reference):
+    # model.hpp:159-201: the device-built CSR against the reference layout
+    for args in [(1000, 10000, 5.0, 0, ("constant", 1.0, 1.0), 7), (300, 150, 4.0, 2, ("uniform", 0.5, 1.5), 3)]:
+        ra = reference.gen(*args).arrays()
+        p = pmp.problem_from_arrays(ra.m, ra.n, ra.capacities, ra.weights, ra.kinds, ra.stream_offsets, ra.route_links)
+        with pmp.PmpSolver(p) as s:
+            lo, lt, lc = s.export_layout()
+        np.testing.assert_array_equal(lo, ra.link_offsets)
+        np.testing.assert_array_equal(lt, ra.link_terminals)
+        np.testing.assert_array_equal(lc, ra.link_counts)
+
+
+def test_layout_transit_unsorted_routes(reference):
+    # config E shape (small): routes in travel order, not sorted
+    rp = reference.gen_transit(12, 24, 5.0, 30, 40, 3, 24, 50.0, 4)
+    ra = rp.arrays()
+    p = pmp.problem_from_arrays(ra.m, ra.n, ra.capacities, ra.weights, ra.kinds, ra.stream_offsets, ra.route_links)
+    with pmp.PmpSolver(p) as s:
+        lo, lt, lc = s.export_layout()
+    np.testing.assert_array_equal(lo, ra.link_offsets)
+    np.testing.assert_array_equal(lt, ra.link_terminals)
+    np.testing.assert_array_equal(lc, ra.link_counts)
+
+
+def test_transit_solve_matches_reference(reference):
+    rp = reference.gen_transit(12, 24, 5.0, 30, 40, 3, 24, 50.0, 4)
+    ra = rp.arrays()
+    p = pmp.problem_from_arrays(ra.m, ra.n, ra.capacities, ra.weights, ra.kinds, ra.stream_offsets, ra.route_links)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1.0, max_iters=3000)
+    from oracle.oracle import Config
+
+    ref = rp.solve(Config(eps_abs=1e-5, rho0=1.0, max_iters=3000))
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    assert sol.iterations == ref.iterations
+    ok, err = close(sol.x, ref.x)
+    assert ok, err
+
+
+def test_runs_are_bit_identical():
+    # determinism (parallel.hpp:54-76, test_solver.cpp:474-492): fixed-order device reductions
+    p = _gen(2000, 4000, 6.0, 2, True, 11)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    with pmp.PmpSolver(p, cfg) as s:
+        a = s.solve()
+        b = s.solve()
+    assert a.iterations == b.iterations
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
+    assert a.r_norm == b.r_norm and a.s_norm == b.s_norm
+
+
+def test_extension_streams_rejected():
+    p = pmp.problem_from_arrays(1, 1, [1.0], [1.0], [2], [0, 1], [0])
+    with pytest.raises(pmp.SolverError):
+        pmp.PmpSolver(p)
+
+
+def test_config_validation():
+    p = single()
+    for bad in [dict(eps_abs=0.0), dict(rho0=-1.0), dict(alpha=2.5), dict(mu=1.0), dict(gamma=1.0),
+                dict(rho_update_interval=0), dict(max_iters=0), dict(trace_every=0), dict(threads=-1),
+                dict(time_limit=-1.0)]:
+        with pytest.raises(ValueError):
+            pmp.PmpSolver(p, pmp.SolverConfig(**bad))
+
+
+# ------------------------------------------------------------- config B / C
+@pytest.mark.slow
+def test_config_b_iterations_match_oracle(restatement, oracle_mod):
+    # BASELINE.json configs[1]: 1M streams / 100k links, log utilities
+    p = _gen(100000, 1000000, 10.0, 0, False, 7)
+    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0, max_iters=20)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations == 20
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw)]:
+        ok, err = close(got, want)
+        assert ok, err
+    for row, want in zip(sol.trace, ref.trace):
+        assert abs(row.r_norm - want[1]) <= RTOL * want[1] and abs(row.s_norm - want[2]) <= RTOL * want[2]
+
+
+@pytest.mark.slow
+def test_config_c_full_solve_properties():
+    # BASELINE.json configs[2] at full size: converged run is feasible within
+    # tolerance and satisfies complementary slackness (test_solver.cpp:417-472)
+    p = _gen(1000000, 10000000, 10.0, 2, True, 7)
+    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    assert sol.status == pmp.SolveStatus.Converged
+    eps_tol = 1e-4 * math.sqrt(p.nnz + p.m)
+    load = np.bincount(p.route_links, weights=np.repeat(sol.x, np.diff(p.stream_offsets)), minlength=p.m)
+    viol = load + sol.s - p.capacities
+    assert np.max(np.abs(viol)) <= 10.0 * eps_tol
+    assert np.min(sol.x) >= -1e-4
+    assert np.min(sol.lambda_) >= 0.0
