@@ -4,6 +4,7 @@
 //
 // Reference boundary replaced: numpmp::PmpSolver (solver.hpp:265-519).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -40,11 +41,49 @@ struct GpuError {
     if (e_ != cudaSuccess)                                                                 \
       throw GpuError{NUMPMP_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
   } while (0)
+// NCCL is resolved lazily with dlopen, only for sharded (multi-GPU)
+// handles: the single-GPU path never loads it, and a process that already
+// loaded an NCCL (e.g. PyTorch's bundled one, for torch.distributed) shares
+// that copy instead of pulling in a second, older libnccl.so.2.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(lib, "ncclCommInitRank"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(lib, "ncclAllReduce"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(lib, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(lib, "ncclGetErrorString"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.GetErrorString)
+      a.error = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  if (!api.error.empty()) throw GpuError{NUMPMP_NCCL_ERROR, api.error};
+  return api;
+}
+
 #define NK(call)                                                                           \
   do {                                                                                     \
-    ncclResult_t r_ = (call);                                                              \
+    const NcclApi& api_ = nccl();                                                          \
+    ncclResult_t r_ = (api_.call);                                                         \
     if (r_ != ncclSuccess)                                                                 \
-      throw GpuError{NUMPMP_NCCL_ERROR, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+      throw GpuError{NUMPMP_NCCL_ERROR, std::string(#call) + ": " + api_.GetErrorString(r_)}; \
   } while (0)
 
 thread_local std::string g_create_err;
@@ -216,7 +255,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t ev_start
   } else {
     k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a);
     CK(cudaGetLastError());
-    NK(ncclAllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum,
+    NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum,
                      h->comm, h->stream));
     k_link_pass<LP_EPILOGUE><<<h->grid2, kThreads, 0, h->stream>>>(a);
   }
@@ -269,7 +308,7 @@ void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
   k_row_sums<<<h->grid2, kThreads, 0, h->stream>>>(h->row_ptr, h->col_idx, src, h->m, out);
   CK(cudaGetLastError());
   if (h->sharded)
-    NK(ncclAllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm,
+    NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm,
                      h->stream));
 }
 
@@ -471,8 +510,11 @@ const char* numpmp_gpu_last_error(const numpmp_gpu* h) {
 
 int numpmp_gpu_nccl_unique_id(void* out128) {
   ncclUniqueId id;
-  ncclResult_t r = ncclGetUniqueId(&id);
-  if (r != ncclSuccess) return set_err(nullptr, NUMPMP_NCCL_ERROR, ncclGetErrorString(r));
+  try {
+    NK(GetUniqueId(&id));
+  } catch (const GpuError& e) {
+    return set_err(nullptr, e.code, e.msg);
+  }
   std::memcpy(out128, &id, sizeof(id));
   return NUMPMP_OK;
 }
@@ -518,7 +560,7 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
       CK(cudaSetDevice(device));
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
-      NK(ncclCommInitRank(&h->comm, world, id, rank));
+      NK(CommInitRank(&h->comm, world, id, rank));
     }
     create_common(h, pv);
     if (h->sharded) {
@@ -526,11 +568,11 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
       h->deg = dalloc<int>(static_cast<size_t>(h->m), &h->dev_bytes);
       k_degree<<<grid_for(h->m), 256, 0, h->stream>>>(h->row_ptr, h->m, h->deg);
       CK(cudaGetLastError());
-      NK(ncclAllReduce(h->deg, h->deg, static_cast<size_t>(h->m), ncclInt32, ncclSum, h->comm,
+      NK(AllReduce(h->deg, h->deg, static_cast<size_t>(h->m), ncclInt32, ncclSum, h->comm,
                        h->stream));
       double nnz_local = static_cast<double>(h->nnz);
       CK(cudaMemcpyAsync(h->scalars, &nnz_local, 8, cudaMemcpyHostToDevice, h->stream));
-      NK(ncclAllReduce(h->scalars, h->scalars, 1, ncclDouble, ncclSum, h->comm, h->stream));
+      NK(AllReduce(h->scalars, h->scalars, 1, ncclDouble, ncclSum, h->comm, h->stream));
       double nnz_global = 0.0;
       CK(cudaMemcpyAsync(&nnz_global, h->scalars, 8, cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));
@@ -836,7 +878,7 @@ void post_process(numpmp_gpu* h, double* x, double* s, double* lambda, double* l
   k_sum_parts<<<1, kThreads, 0, h->stream>>>(h->k1_part, gpost, h->scalars);
   CK(cudaGetLastError());
   if (h->sharded)
-    NK(ncclAllReduce(h->scalars, h->scalars, 2, ncclDouble, ncclSum, h->comm, h->stream));
+    NK(AllReduce(h->scalars, h->scalars, 2, ncclDouble, ncclSum, h->comm, h->stream));
   global_row_sums(h, h->scratch_n, h->scratch_m);  // load = R x (clamped x)
   k_post_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->cap, h->pr[cu], h->m,
                                                       h->scratch_m2, h->Lbuf);
@@ -1003,7 +1045,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
                   h->scalars, h->ctrl,    h->trace_dev};
   for (void* p : bufs) cudaFree(p);
   if (h->ctrl_host) cudaFreeHost(h->ctrl_host);
-  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->comm) nccl().CommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
