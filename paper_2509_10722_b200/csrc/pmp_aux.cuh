@@ -14,19 +14,25 @@ __global__ void k_offsets_to_i32(const long long* __restrict__ in, int* __restri
     out[i] = static_cast<int>(in[i]);
 }
 
-// terminal -> stream map and terminal iota (sort values).
-__global__ void k_terminal_stream(const int* __restrict__ col_ptr, long long n,
+// terminal -> (global) stream map for the streams col_ptr[0..n) (absolute
+// terminal ids), and the terminal iota used as sort values.
+__global__ void k_terminal_stream(const int* __restrict__ col_ptr, long long n, long long s0,
                                   int* __restrict__ t2s) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
        j += (long long)gridDim.x * blockDim.x) {
     const int b = col_ptr[j], e = col_ptr[j + 1];
-    for (int t = b; t < e; ++t) t2s[t] = static_cast<int>(j);
+    for (int t = b; t < e; ++t) t2s[t] = static_cast<int>(s0 + j);
   }
 }
-__global__ void k_iota(int* __restrict__ out, long long count) {
+__global__ void k_iota(int* __restrict__ out, long long count, long long base) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x)
-    out[i] = static_cast<int>(i);
+    out[i] = static_cast<int>(base + i);
+}
+__global__ void k_add_degree(const int* __restrict__ row_ptr, long long m, int* __restrict__ deg) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x)
+    deg[l] += row_ptr[l + 1] - row_ptr[l];
 }
 // Row pointer from the link-sorted keys: row_ptr[l] = first k with key >= l.
 __global__ void k_row_ptr_from_sorted(const int* __restrict__ keys, long long nnz, long long m,
@@ -50,13 +56,14 @@ __global__ void k_degree(const int* __restrict__ row_ptr, long long m, int* __re
     deg[l] = row_ptr[l + 1] - row_ptr[l];
 }
 
-// Sequential per-row sums L_l = sum_{j in row l} src_j (ascending stream
-// order) -- the same arithmetic as the link pass.
+// Per-row sums over one column block, accumulated across blocks in block
+// order: out = (first ? 0 : out) + sum_{j in row l, block b} src_j -- the
+// same arithmetic and order as the link pass.
 __global__ void __launch_bounds__(kThreads) k_row_sums(const int* __restrict__ row_ptr,
                                                        const int* __restrict__ col_idx,
                                                        const double* __restrict__ src, long long m,
-                                                       double* __restrict__ out) {
-  __shared__ double sbuf[kWarps][kChunk];
+                                                       double* __restrict__ out, int first) {
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
   const long long ngroups = (m + 31) / 32;
@@ -67,8 +74,8 @@ __global__ void __launch_bounds__(kThreads) k_row_sums(const int* __restrict__ r
     const int rb = row_ptr[valid ? r : m];
     const int re = valid ? row_ptr[r + 1] : rb;
     const int sb = __shfl_sync(kFull, rb, 0), se = __shfl_sync(kFull, re, 31);
-    const double L = warp_segmented_sum(col_idx, sb, se, rb, re, sbuf[wib], lane, GatherX{src}, pol);
-    if (valid) out[r] = L;
+    const double s = warp_segments_sum(col_idx, sb, se, rb, re, sidx[wib], lane, GatherX{src}, pol);
+    if (valid) out[r] = first ? s : out[r] + s;
   }
 }
 

@@ -8,15 +8,15 @@
 // device keeps only stream-space (A, x) and link-space (B, zs, price, Q, v)
 // vectors:
 //
-//   v_l   = B_l + price_l / rho                        (written by K2)
-//   zeta_j = tau_j A_j - sum_{l in route(j)} v_l        (K1, route order)
-//   x_j   = prox(zeta_j)                  (prox.hpp:31-56, IEEE sqrt/div)
-//   A_j  <- alpha x_j + (1 - alpha) A_j
-//   ps_l  = max(zs_l - price_l/rho, -c_l)              (K2 epilogue)
-//   L_l   = sum_{j in link l} x_j    (ascending stream id, sequential)
-//   pbar_l = (L_l + ps_l) / (d_l + 1)   == compute_link_averages bit for bit
-//   B_l  <- alpha pbar_l + (1 - alpha) B_l
-//   zs_l <- alpha (ps_l - pbar_l) + (1 - alpha) zs_l
+//   v_l    = B_l + price_l / rho                       (link epilogue)
+//   zeta_j = tau_j A_j - sum_{l in route(j)} v_l        (stream pass, route order)
+//   x_j    = prox(zeta_j)                 (prox.hpp:31-56, IEEE sqrt/div)
+//   A_j   <- alpha x_j + (1 - alpha) A_j
+//   ps_l   = max(zs_l - price_l/rho, -c_l)             (link epilogue)
+//   L_l    = sum_{j in link l} x_j        (ascending stream id)
+//   pbar_l = (L_l + ps_l) / (d_l + 1)
+//   B_l   <- alpha pbar_l + (1 - alpha) B_l
+//   zs_l  <- alpha (ps_l - pbar_l) + (1 - alpha) zs_l
 //   price_l += rho (alpha pbar_l)
 //   r^2 = sum_l (d_l + 1) pbar_l^2
 //   s^2 = rho^2 [ sum_j tau_j dA_j^2 - 2 sum_l dB_l (R dA)_l
@@ -26,10 +26,14 @@
 // state, Q <- alpha L + (1 - alpha) Q, so (R dA)_l = Q_new - Q_old.  The
 // tracking error is damped by |1 - alpha| <= 1 every iteration.
 //
-// Kernels per iteration: K1 (stream pass over the CSC, R^T v gather + prox)
-// and K2 (link pass over the CSR, R x gather + link epilogue + residual
-// partials; its last block finalizes r, s, termination, trace and rho
-// balancing on the device, solver.hpp:450-476).  No host sync per iteration.
+// Both passes are bound by random 8-byte gathers (one per nonzero and
+// direction), i.e. by the L1TEX wavefront rate, not by HBM bytes.  The
+// gather core therefore stages only the 32-bit *indices* of a warp's span in
+// shared memory (coalesced 128-bit loads, conflict-free 128-bit stores) and
+// lets every lane gather and sum its own segment in registers, in index
+// order.  Column blocks: the streams are split into NB contiguous blocks;
+// the stream pass over block b is followed immediately by the link-pass
+// gather over block b's CSR, so the just-written x_b is still L2-resident.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -39,10 +43,10 @@
 
 namespace numpmp_dev {
 
-constexpr int kWarps = 8;                 // warps per block (gather passes)
+constexpr int kWarps = 8;  // warps per block (gather passes)
 constexpr int kThreads = kWarps * 32;
-constexpr int kChunk = 256;               // staged nonzeros per warp and round
-constexpr int kGroupsPerLane = kChunk / 128;  // int4 index groups per lane
+constexpr int kMinBlocks = 4;  // resident blocks per SM the gather passes are built for (<= 64 regs)
+constexpr int kStageInts = 512;  // staged indices per warp and round (2 KB)
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { ST_RUNNING = -1, ST_CONVERGED = 0, ST_MAXITERS = 1, ST_TIMELIMIT = 2,
@@ -62,7 +66,7 @@ struct Ctrl {
   long long t0_ns;   // %globaltimer at the start of the run
   int done;          // 1: every later kernel of the batch exits at entry
   int status;        // ST_*
-  int rho_changed;   // next K1 recomputes v = B + price / rho
+  int rho_changed;   // next stream pass recomputes v = B + price / rho
   unsigned ticket;   // last-block detection, link pass
   unsigned ticket2;  // last-block detection, sharded gather pass
   int pad;
@@ -70,15 +74,12 @@ struct Ctrl {
 
 struct IterArgs {
   // stream side (CSC of R)
-  const int* col_ptr;      // n+1
-  const int* row_idx;      // nnz (+pad), link of each terminal in route order
-  const double* w;         // n
+  const int* col_ptr;         // n+1
+  const int* row_idx;         // nnz (+pad), link of each terminal in route order
+  const double* w;            // n
   const unsigned char* kind;  // n
-  // link side (CSR of R, rows = links, ascending local stream ids)
-  const int* row_ptr;      // m+1
-  const int* col_idx;      // nnz (+pad)
-  const int* deg;          // m, global degree (sharded); null -> row_ptr diff
-  const double* cap;       // m
+  const int* deg;             // m, link degree (global)
+  const double* cap;          // m
   long long n, m;
   // config
   double alpha, eps_tol, mu, gamma;
@@ -97,13 +98,23 @@ struct IterArgs {
   const double* Q_in;
   double* Q_out;
   double* v;
-  double* k1_part;         // [grid1][2]: tau dA^2, objective
-  double* k2_part;         // [grid2][4]: r^2, dB.dQ, d dB^2, dzs^2
-  int grid1, grid2;
-  double* Lbuf;            // sharded: m partial loads + 2 scalars
+  double* k1_part;  // [nb][grid1][2]: tau dA^2, objective
+  double* k2_part;  // [grid2][4]: r^2, dB.dQ, d dB^2, dzs^2
+  int grid1, grid2, nblocks;
+  double* Lacc;     // m: running sum of the column blocks' partial loads
+  double* Lbuf;     // sharded: m partial loads + 2 scalars
   Ctrl* ctrl;
   numpmp_trace_row* trace;
   long long trace_cap;
+};
+
+// One column block: streams [s0, s1) and the CSR of their columns.
+struct BlockArgs {
+  long long s0, s1;
+  const int* row_ptr;  // m+1 into col_idx
+  const int* col_idx;  // global stream ids, ascending per row
+  int index;           // block number b
+  int first;           // b == 0
 };
 
 // ---------------------------------------------------------------- helpers
@@ -129,6 +140,11 @@ __device__ __forceinline__ int4 ld_stream_int4(const int* p, uint64_t pol) {
 __device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
   double r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_gather_f64(const double* p) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void st_hint_f64(double* p, double v, uint64_t pol) {
@@ -176,57 +192,59 @@ struct GatherBU {  // v_l recomputed after a rho change / state upload
 };
 struct GatherX {  // x_j (written by this iteration's stream pass)
   const double* __restrict__ x;
-  __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j); }
+  __device__ __forceinline__ double operator()(int j) const { return ld_gather_f64(x + j); }
 };
 
 // Warp-cooperative segmented gather-sum.  The 32 lanes own contiguous,
 // lane-ordered segments [seg_beg, seg_end) tiling [span_beg, span_end) of
-// the index array.  The span is streamed with coalesced 128-bit index
-// loads, the gathered values are staged in shared memory, and each lane
-// then adds its own segment sequentially in index order -- the summation
-// order of the reference (route order for R^T v, ascending stream id for
-// R x), so link averages are bit-identical to compute_link_averages given
-// the same x.
+// the index array.  Rounds of kStageInts indices are streamed with
+// coalesced 128-bit loads (the next round is prefetched into registers
+// while the current one is gathered) and parked in shared memory; each lane
+// then reads its own indices back and gathers/sums its segment in
+// registers, in index order (route order for R^T v, ascending stream id for
+// R x), four gathers in flight.
 template <class G>
-__device__ __forceinline__ double warp_segmented_sum(const int* __restrict__ idx, int span_beg,
-                                                     int span_end, int seg_beg, int seg_end,
-                                                     double* __restrict__ sbuf, int lane, G g,
-                                                     uint64_t pol_stream) {
+__device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx, int span_beg,
+                                                    int span_end, int seg_beg, int seg_end,
+                                                    int* __restrict__ sidx, int lane, G g,
+                                                    uint64_t pol_stream) {
+  constexpr int NV = kStageInts / 128;
   double acc = 0.0;
-  const int base0 = span_beg & ~3;
-  for (int cb = base0; cb < span_end; cb += kChunk) {
-    const int c0 = max(cb, span_beg);
-    const int c1 = min(cb + kChunk, span_end);
-    int4 iv[kGroupsPerLane];
+  int cb = span_beg & ~3;
+  int4 buf[NV];
 #pragma unroll
-    for (int i = 0; i < kGroupsPerLane; ++i) {
-      const int gpos = cb + 4 * (lane + 32 * i);
-      if (gpos < c1) iv[i] = ld_stream_int4(idx + gpos, pol_stream);
-    }
-    double vals[kGroupsPerLane][4];
+  for (int i = 0; i < NV; ++i) {
+    const int gp = cb + 4 * (lane + 32 * i);
+    if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
+  }
+  while (cb < span_end) {
+    const int c1 = min(cb + kStageInts, span_end);
 #pragma unroll
-    for (int i = 0; i < kGroupsPerLane; ++i) {
-      const int gpos = cb + 4 * (lane + 32 * i);
-      const int e[4] = {iv[i].x, iv[i].y, iv[i].z, iv[i].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int pos = gpos + q;
-        vals[i][q] = (pos >= c0 && pos < c1) ? g(e[q]) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < kGroupsPerLane; ++i) {
-      const int gpos = cb + 4 * (lane + 32 * i);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int pos = gpos + q;
-        if (pos >= c0 && pos < c1) sbuf[pos - cb] = vals[i][q];
-      }
+    for (int i = 0; i < NV; ++i) {
+      const int o = 4 * (lane + 32 * i);
+      if (cb + o < c1) *reinterpret_cast<int4*>(sidx + o) = buf[i];
     }
     __syncwarp();
-    const int lo = max(seg_beg, c0), hi = min(seg_end, c1);
-    for (int k = lo; k < hi; ++k) acc += sbuf[k - cb];
+    const int nb = cb + kStageInts;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int gp = nb + 4 * (lane + 32 * i);
+      if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
+    }
+    const int lo = max(seg_beg, cb), hi = min(seg_end, c1);
+    int k = lo;
+    for (; k + 4 <= hi; k += 4) {
+      const int i0 = sidx[k - cb], i1 = sidx[k + 1 - cb], i2 = sidx[k + 2 - cb],
+                i3 = sidx[k + 3 - cb];
+      const double v0 = g(i0), v1 = g(i1), v2 = g(i2), v3 = g(i3);
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; k < hi; ++k) acc += g(sidx[k - cb]);
     __syncwarp();
+    cb = nb;
   }
   return acc;
 }
@@ -280,30 +298,36 @@ __device__ __forceinline__ bool kernel_should_exit(const Ctrl* ctrl) {
 }
 
 // ------------------------------------------------------------ K1: streams
-// R^T v gather over the CSC + prox + A update (solver.hpp:325-366 restated).
+// R^T v gather over the CSC + prox + A update (solver.hpp:325-366
+// restated), for the streams of one column block.
 template <class G>
-__device__ __forceinline__ void stream_pass_body(const IterArgs& a, G g, double rho, bool trace_it,
-                                                 double* sbuf, double& p_tda2, double& p_obj) {
+__device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockArgs& bk, G g,
+                                                 double rho, bool trace_it, int* sidx,
+                                                 double& p_tda2, double& p_obj) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
-  const long long ntiles = (a.n + 31) / 32;
+  const long long ntiles = (bk.s1 - bk.s0 + 31) / 32;
   const double alpha = a.alpha;
   for (long long tile = (long long)blockIdx.x * kWarps + wib; tile < ntiles;
        tile += (long long)gridDim.x * kWarps) {
-    const long long j = tile * 32 + lane;
-    const bool valid = j < a.n;
-    const int beg = __ldg(a.col_ptr + (valid ? j : a.n));
+    const long long j = bk.s0 + tile * 32 + lane;
+    const bool valid = j < bk.s1;
+    const int beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
     const int end = valid ? __ldg(a.col_ptr + j + 1) : beg;
+    double A = 0.0, w = 0.0;
+    int kd = 0;
+    if (valid) {  // independent of the gather: issue early
+      A = ld_stream_f64(a.A_in + j, pol_first);
+      w = __ldg(a.w + j);
+      kd = __ldg(a.kind + j);
+    }
     const int span_beg = __shfl_sync(kFull, beg, 0);
     const int span_end = __shfl_sync(kFull, end, 31);
-    const double sum = warp_segmented_sum(a.row_idx, span_beg, span_end, beg, end, sbuf, lane, g,
-                                          pol_first);
+    const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
+                                         pol_first);
     if (valid) {
       const int tau = end - beg;
-      const double A = ld_stream_f64(a.A_in + j, pol_first);
-      const double w = __ldg(a.w + j);
-      const int kd = __ldg(a.kind + j);
       const double zeta = static_cast<double>(tau) * A - sum;
       const double x = (kd == NUMPMP_KIND_LOG) ? prox_log(zeta, w, rho, tau)
                                                : prox_linear_nonneg(zeta, w, rho, tau);
@@ -317,27 +341,28 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, G g, double 
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_stream_pass(IterArgs a) {
-  __shared__ double sbuf[kWarps][kChunk];
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
   const bool rc = a.ctrl->rho_changed != 0;
   const long long k = a.ctrl->run_k + 1;
   const bool trace_it = (a.mode == MODE_RUN) && (k % a.trace_every == 0);
   double part[2] = {0.0, 0.0};
-  double* sb = sbuf[threadIdx.x >> 5];
+  int* sb = sidx[threadIdx.x >> 5];
   if (rc)
-    stream_pass_body(a, GatherBU{a.B_in, a.pr_in, rho}, rho, trace_it, sb, part[0], part[1]);
+    stream_pass_body(a, bk, GatherBU{a.B_in, a.pr_in, rho}, rho, trace_it, sb, part[0], part[1]);
   else
-    stream_pass_body(a, GatherV{a.v}, rho, trace_it, sb, part[0], part[1]);
-  block_sum_store<2>(part, a.k1_part + 2 * blockIdx.x);
+    stream_pass_body(a, bk, GatherV{a.v}, rho, trace_it, sb, part[0], part[1]);
+  block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 
 // --------------------------------------------------------------- K2: links
 // Per-link epilogue: slack projection (solver.hpp:368-376), link average
 // (110-126), z update split into B / zs / Q (388-399), price (401-405).
 __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, double L, int d,
-                                              double rho, double (&part)[4], uint64_t pol) {
+                                              double rho, double (&part)[4], uint64_t pol,
+                                              uint64_t pol_last) {
   const double alpha = a.alpha;
   const double c = __ldg(a.cap + r);
   const double pr = ld_stream_f64(a.pr_in + r, pol);
@@ -363,7 +388,7 @@ __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, do
   a.zs_out[r] = zsn;
   a.Q_out[r] = Qn;
   a.pr_out[r] = prn;
-  a.v[r] = Bn + prn / rho;
+  st_hint_f64(a.v + r, Bn + prn / rho, pol_last);
 }
 
 // Finalize one iteration on the device: r, s, then the exact control order
@@ -421,19 +446,24 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
   }
 }
 
-enum : int { LP_FUSED = 0, LP_GATHER = 1, LP_EPILOGUE = 2 };
+// Link-pass phases.
+//   LP_ACC      : gather over column block b, L partial -> Lacc (b < NB-1).
+//   LP_FUSED    : gather over the last block, L = Lacc + partial, epilogue,
+//                 residual partials, last-block finalize (single GPU).
+//   LP_GATHER   : sharded, last block: local loads -> Lbuf (+ K1 scalars),
+//                 then the NCCL all-reduce.
+//   LP_EPILOGUE : sharded, replicated epilogue on the all-reduced loads.
+enum : int { LP_ACC = 0, LP_FUSED = 1, LP_GATHER = 2, LP_EPILOGUE = 3 };
 
-// LP_FUSED: single GPU, gather + epilogue + finalize.
-// LP_GATHER: sharded, local partial loads -> Lbuf (+ K1 scalars), then NCCL.
-// LP_EPILOGUE: sharded, replicated epilogue on the all-reduced loads.
 template <int kPhase>
-__global__ void __launch_bounds__(kThreads) k_link_pass(IterArgs a) {
-  __shared__ double sbuf[kWarps][kChunk];
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk) {
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   __shared__ bool s_last;
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last();
   const long long ngroups = (a.m + 31) / 32;
   double part[4] = {0.0, 0.0, 0.0, 0.0};
   for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
@@ -441,27 +471,32 @@ __global__ void __launch_bounds__(kThreads) k_link_pass(IterArgs a) {
     const long long r = g * 32 + lane;
     const bool valid = r < a.m;
     double L;
-    int d;
     if (kPhase == LP_EPILOGUE) {
       if (!valid) continue;
       L = __ldcg(a.Lbuf + r);
-      d = __ldg(a.deg + r);
     } else {
-      const int rb = __ldg(a.row_ptr + (valid ? r : a.m));
-      const int re = valid ? __ldg(a.row_ptr + r + 1) : rb;
+      const int rb = __ldg(bk.row_ptr + (valid ? r : a.m));
+      const int re = valid ? __ldg(bk.row_ptr + r + 1) : rb;
+      double prev = 0.0;
+      if (!bk.first && valid) prev = __ldcg(a.Lacc + r);
       const int span_beg = __shfl_sync(kFull, rb, 0);
       const int span_end = __shfl_sync(kFull, re, 31);
-      L = warp_segmented_sum(a.col_idx, span_beg, span_end, rb, re, sbuf[wib], lane,
-                             GatherX{a.x}, pol_first);
-      d = re - rb;
+      const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
+                                         GatherX{a.x}, pol_first);
       if (!valid) continue;
+      L = bk.first ? s : prev + s;
+      if (kPhase == LP_ACC) {
+        __stcg(a.Lacc + r, L);
+        continue;
+      }
       if (kPhase == LP_GATHER) {
         a.Lbuf[r] = L;
         continue;
       }
     }
-    link_epilogue(a, r, L, d, rho, part, pol_first);
+    link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
   }
+  if (kPhase == LP_ACC) return;
   if (kPhase == LP_GATHER) {
     // The last block folds K1's scalar partials into Lbuf[m], Lbuf[m+1] so
     // one all-reduce carries loads and scalars.
@@ -471,8 +506,8 @@ __global__ void __launch_bounds__(kThreads) k_link_pass(IterArgs a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const double tda2 = block_sum_array(a.k1_part, a.grid1, 2, 0);
-    const double obj = block_sum_array(a.k1_part, a.grid1, 2, 1);
+    const double tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
+    const double obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
     if (threadIdx.x == 0) {
       a.Lbuf[a.m] = tda2;
       a.Lbuf[a.m + 1] = obj;
@@ -491,8 +526,8 @@ __global__ void __launch_bounds__(kThreads) k_link_pass(IterArgs a) {
     tda2 = __ldcg(a.Lbuf + a.m);
     obj = __ldcg(a.Lbuf + a.m + 1);
   } else {
-    tda2 = block_sum_array(a.k1_part, a.grid1, 2, 0);
-    obj = block_sum_array(a.k1_part, a.grid1, 2, 1);
+    tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
+    obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
   }
   const double r2 = block_sum_array(a.k2_part, a.grid2, 4, 0);
   const double cross = block_sum_array(a.k2_part, a.grid2, 4, 1);

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -104,6 +105,13 @@ int grid_for(long long work, int threads = 256) {
   return static_cast<int>(b);
 }
 
+// One column block of the device problem (see pmp_kernels.cuh).
+struct ColBlock {
+  int64_t s0 = 0, s1 = 0, nnz = 0;
+  int* row_ptr = nullptr;  // m+1
+  int* col_idx = nullptr;  // nnz + pad, global stream ids
+};
+
 }  // namespace
 
 struct numpmp_gpu {
@@ -123,10 +131,9 @@ struct numpmp_gpu {
   int* row_idx = nullptr;
   double* w = nullptr;
   unsigned char* kind = nullptr;
-  int* row_ptr = nullptr;
-  int* col_idx = nullptr;
-  int* deg = nullptr;  // global link degrees (sharded only)
+  int* deg = nullptr;  // link degrees (global)
   double* cap = nullptr;
+  std::vector<ColBlock> blocks;
 
   // state (ping-pong between iterations)
   double* A[2] = {nullptr, nullptr};
@@ -138,6 +145,7 @@ struct numpmp_gpu {
   double* v = nullptr;
   double* ps0 = nullptr;    // slack flows of an uploaded state
   double* pbar0 = nullptr;  // link averages of an uploaded state
+  double* Lacc = nullptr;   // m
   double* Lbuf = nullptr;   // m + 2
   double* k1_part = nullptr;
   double* k2_part = nullptr;
@@ -162,13 +170,17 @@ struct numpmp_gpu {
   cudaGraphExec_t prof_graph[2] = {nullptr, nullptr};
   cudaEvent_t ev_batch[2] = {nullptr, nullptr};
   bool profiling = false;
-  std::vector<cudaEvent_t> prof_ev;  // 2 * kBatchIters + 1
+  std::vector<cudaEvent_t> prof_ev;  // 1 + kBatchIters * launches_per_iteration
   int64_t prof_launches = 0, prof_iters = 0;
   double prof_ms_k1 = 0.0, prof_ms_k2 = 0.0;
 
   int64_t h2d = 0, d2h = 0;
   cudaEvent_t ev_run[2] = {nullptr, nullptr};
   double last_run_ms = 0.0;
+
+  int nb() const { return static_cast<int>(blocks.size()); }
+  // kernel launches of one iteration (the NCCL all-reduce is not ours)
+  int launches_per_iteration() const { return 2 * nb() + (sharded ? 1 : 0); }
 };
 
 namespace {
@@ -200,8 +212,6 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.row_idx = h->row_idx;
   a.w = h->w;
   a.kind = h->kind;
-  a.row_ptr = h->row_ptr;
-  a.col_idx = h->col_idx;
   a.deg = h->deg;
   a.cap = h->cap;
   a.n = h->n;
@@ -233,6 +243,8 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.k2_part = h->k2_part;
   a.grid1 = h->grid1;
   a.grid2 = h->grid2;
+  a.nblocks = h->nb();
+  a.Lacc = h->Lacc;
   a.Lbuf = h->Lbuf;
   a.ctrl = h->ctrl;
   a.trace = h->trace_dev;
@@ -240,42 +252,65 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   return a;
 }
 
-// One PMP iteration on the stream: K1, then K2 (fused) or K2a + NCCL
-// all-reduce of the partial link loads + K2b (sharded).  Optional events:
-// ev_start (before K1, may be null), ev_mid (after K1), ev_end (after K2).
-void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t ev_start,
-                       cudaEvent_t ev_mid, cudaEvent_t ev_end) {
+BlockArgs block_args(const numpmp_gpu* h, int b) {
+  const ColBlock& cb = h->blocks[static_cast<size_t>(b)];
+  BlockArgs k{};
+  k.s0 = cb.s0;
+  k.s1 = cb.s1;
+  k.row_ptr = cb.row_ptr;
+  k.col_idx = cb.col_idx;
+  k.index = b;
+  k.first = b == 0;
+  return k;
+}
+
+// One PMP iteration on the stream: for each column block b the stream pass
+// K1(b) and the link-pass gather K2(b); the last block's link pass is fused
+// with the link epilogue and the device-side finalize (single GPU), or
+// followed by the NCCL all-reduce of the partial loads and the replicated
+// epilogue (sharded).  ev (nullable): events[0..launches] recorded around
+// every launch; ev[0] is skipped when record_first is false.
+void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, bool record_first) {
   IterArgs a = make_args(h, parity, mode);
-  if (ev_start) CK(cudaEventRecordWithFlags(ev_start, h->stream, cudaEventRecordExternal));
-  k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a);
-  CK(cudaGetLastError());
-  if (ev_mid) CK(cudaEventRecordWithFlags(ev_mid, h->stream, cudaEventRecordExternal));
-  if (!h->sharded) {
-    k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a);
-  } else {
-    k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a);
+  int e = 0;
+  auto mark = [&]() {
+    if (ev) CK(cudaEventRecordWithFlags(ev[e], h->stream, cudaEventRecordExternal));
+    ++e;
+  };
+  if (record_first) mark();
+  else ++e;
+  const int nb = h->nb();
+  for (int b = 0; b < nb; ++b) {
+    const BlockArgs bk = block_args(h, b);
+    k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
     CK(cudaGetLastError());
-    NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum,
-                     h->comm, h->stream));
-    k_link_pass<LP_EPILOGUE><<<h->grid2, kThreads, 0, h->stream>>>(a);
+    mark();
+    if (b + 1 < nb)
+      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk);
+    else if (!h->sharded)
+      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk);
+    else
+      k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk);
+    CK(cudaGetLastError());
+    mark();
   }
-  CK(cudaGetLastError());
-  if (ev_end) CK(cudaEventRecordWithFlags(ev_end, h->stream, cudaEventRecordExternal));
+  if (h->sharded) {
+    NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum, h->comm,
+                 h->stream));
+    k_link_pass<LP_EPILOGUE><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, 0));
+    CK(cudaGetLastError());
+    mark();
+  }
 }
 
 cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, bool with_events) {
   cudaGraph_t g = nullptr;
+  const int lpi = h->launches_per_iteration();
   CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    for (int i = 0; i < kBatchIters; ++i) {
-      cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
-      if (with_events) {
-        e0 = i == 0 ? h->prof_ev[0] : nullptr;
-        e1 = h->prof_ev[static_cast<size_t>(2 * i + 1)];
-        e2 = h->prof_ev[static_cast<size_t>(2 * i + 2)];
-      }
-      enqueue_iteration(h, parity ^ (i & 1), MODE_RUN, e0, e1, e2);
-    }
+    for (int i = 0; i < kBatchIters; ++i)
+      enqueue_iteration(h, parity ^ (i & 1), MODE_RUN,
+                        with_events ? &h->prof_ev[static_cast<size_t>(i * lpi)] : nullptr, i == 0);
   } catch (...) {
     cudaStreamEndCapture(h->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -303,61 +338,68 @@ Ctrl read_ctrl(numpmp_gpu* h) {
   return h->ctrl_host[0];
 }
 
-// Local per-link sums over this device's columns (+ NCCL sum when sharded).
+// Per-link sums of src over this device's columns, block by block in the
+// same order as the link pass (+ NCCL sum when sharded).
 void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
-  k_row_sums<<<h->grid2, kThreads, 0, h->stream>>>(h->row_ptr, h->col_idx, src, h->m, out);
-  CK(cudaGetLastError());
+  for (int b = 0; b < h->nb(); ++b) {
+    const ColBlock& cb = h->blocks[static_cast<size_t>(b)];
+    k_row_sums<<<h->grid2, kThreads, 0, h->stream>>>(cb.row_ptr, cb.col_idx, src, h->m, out, b == 0);
+    CK(cudaGetLastError());
+  }
   if (h->sharded)
-    NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm,
-                     h->stream));
+    NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm, h->stream));
 }
 
-// Link-major CSR of R on the device: a stable radix sort of the terminals
-// by link (stable => ascending terminal, hence ascending stream, within a
-// link, exactly the counting sort of model.hpp:193-199), then column index
-// = the terminal's stream.  sorted_terms_out (nullable, host) receives the
-// terminal ids in CSR order, i.e. the reference's link_terminals without
-// the slack terminals.
-void build_csr(numpmp_gpu* h, int* sorted_terms_out) {
-  const long long nnz = h->nnz;
+// Link-major CSR of the columns [s0, s1) on the device: a stable radix sort
+// of their terminals by link (stable => ascending terminal, hence
+// ascending stream, within a link, exactly the counting sort of
+// model.hpp:193-199), then column index = the terminal's (global) stream.
+// sorted_terms_out (nullable, host) receives the terminal ids in CSR order,
+// i.e. the reference's link_terminals without the slack terminals.
+void build_csr(numpmp_gpu* h, int64_t s0, int64_t s1, int* row_ptr_out, int* col_idx_out,
+               int* sorted_terms_out) {
+  std::vector<int> bounds(2);
+  CK(cudaMemcpy(&bounds[0], h->col_ptr + s0, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&bounds[1], h->col_ptr + s1, 4, cudaMemcpyDeviceToHost));
+  const long long t0 = bounds[0], nnz = bounds[1] - bounds[0], ns = s1 - s0;
   int64_t tmpb = 0;
   int* keys_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
   int* vals_in = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
   int* vals_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
-  int* t2s = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
+  int* t2s = dalloc<int>(static_cast<size_t>(h->nnz) + kIdxPad, &tmpb);
   void* temp = nullptr;
-  try {
-    k_iota<<<grid_for(nnz), 256, 0, h->stream>>>(vals_in, nnz);
-    k_terminal_stream<<<grid_for(h->n), 256, 0, h->stream>>>(h->col_ptr, h->n, t2s);
-    CK(cudaGetLastError());
-    int end_bit = 1;
-    while ((1ll << end_bit) < h->m) ++end_bit;
-    size_t temp_bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, h->row_idx, keys_out, vals_in,
-                                       vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
-    CK(cudaMalloc(&temp, temp_bytes > 0 ? temp_bytes : 1));
-    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, h->row_idx, keys_out, vals_in, vals_out,
-                                       static_cast<int>(nnz), 0, end_bit, h->stream));
-    k_row_ptr_from_sorted<<<grid_for(nnz + 1), 256, 0, h->stream>>>(keys_out, nnz, h->m,
-                                                                      h->row_ptr);
-    k_gather_i32<<<grid_for(nnz), 256, 0, h->stream>>>(t2s, vals_out, h->col_idx, nnz);
-    CK(cudaGetLastError());
-    if (sorted_terms_out)
-      download(h, sorted_terms_out, vals_out, sizeof(int) * static_cast<size_t>(nnz));
-    CK(cudaStreamSynchronize(h->stream));
-  } catch (...) {
+  auto release = [&]() {
     cudaFree(temp);
     cudaFree(keys_out);
     cudaFree(vals_in);
     cudaFree(vals_out);
     cudaFree(t2s);
+  };
+  try {
+    k_iota<<<grid_for(nnz), 256, 0, h->stream>>>(vals_in, nnz, t0);
+    k_terminal_stream<<<grid_for(ns), 256, 0, h->stream>>>(h->col_ptr + s0, ns, s0, t2s);
+    CK(cudaGetLastError());
+    int end_bit = 1;
+    while ((1ll << end_bit) < h->m) ++end_bit;
+    size_t temp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, h->row_idx + t0, keys_out, vals_in,
+                                       vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
+    CK(cudaMalloc(&temp, temp_bytes > 0 ? temp_bytes : 1));
+    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, h->row_idx + t0, keys_out, vals_in,
+                                       vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
+    k_row_ptr_from_sorted<<<grid_for(nnz + 1), 256, 0, h->stream>>>(keys_out, nnz, h->m,
+                                                                      row_ptr_out);
+    k_gather_i32<<<grid_for(nnz), 256, 0, h->stream>>>(t2s, vals_out, col_idx_out, nnz);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(col_idx_out + nnz, 0, sizeof(int) * kIdxPad, h->stream));
+    if (sorted_terms_out)
+      download(h, sorted_terms_out, vals_out, sizeof(int) * static_cast<size_t>(nnz));
+    CK(cudaStreamSynchronize(h->stream));
+  } catch (...) {
+    release();
     throw;
   }
-  cudaFree(temp);
-  cudaFree(keys_out);
-  cudaFree(vals_in);
-  cudaFree(vals_out);
-  cudaFree(t2s);
+  release();
 }
 
 void check_view(const numpmp_problem_view* pv) {
@@ -374,6 +416,21 @@ void check_view(const numpmp_problem_view* pv) {
     throw GpuError{NUMPMP_INVALID_ARGUMENT, "problem exceeds the int32 index range of one device"};
 }
 
+// Column blocking: x of one block should stay L2-resident between its
+// stream pass and its link-pass gather (126 MB L2, shared with the
+// streamed index and state arrays).  NUMPMP_COL_BLOCKS overrides.
+int choose_blocks(int64_t n) {
+  if (const char* env = std::getenv("NUMPMP_COL_BLOCKS")) {
+    const int v = std::atoi(env);
+    if (v >= 1) return static_cast<int>(std::min<int64_t>(v, std::max<int64_t>(1, n / 32)));
+  }
+  const int64_t xbytes = 8 * n;
+  const int64_t target = 24ll << 20;
+  int64_t nb = (xbytes + target - 1) / target;
+  nb = std::max<int64_t>(1, std::min<int64_t>(nb, 16));
+  return static_cast<int>(std::min<int64_t>(nb, std::max<int64_t>(1, n / 32)));
+}
+
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaSetDevice(h->device));
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -381,11 +438,10 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int64_t* b = &h->dev_bytes;
   h->col_ptr = dalloc<int>(static_cast<size_t>(n) + 1, b);
   h->row_idx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, b);
-  h->col_idx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, b);
-  h->row_ptr = dalloc<int>(static_cast<size_t>(m) + 1, b);
   h->w = dalloc<double>(static_cast<size_t>(n), b);
   h->kind = dalloc<unsigned char>(static_cast<size_t>(n), b);
   h->cap = dalloc<double>(static_cast<size_t>(m), b);
+  h->deg = dalloc<int>(static_cast<size_t>(m), b);
   for (int i = 0; i < 2; ++i) {
     h->A[i] = dalloc<double>(static_cast<size_t>(n), b);
     h->B[i] = dalloc<double>(static_cast<size_t>(m), b);
@@ -397,6 +453,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->v = dalloc<double>(static_cast<size_t>(m), b);
   h->ps0 = dalloc<double>(static_cast<size_t>(m), b);
   h->pbar0 = dalloc<double>(static_cast<size_t>(m), b);
+  h->Lacc = dalloc<double>(static_cast<size_t>(m), b);
   h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b);
   h->scratch_m = dalloc<double>(static_cast<size_t>(m), b);
   h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b);
@@ -405,7 +462,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->ctrl = dalloc<Ctrl>(1, b);
   CK(cudaMallocHost(&h->ctrl_host, 2 * sizeof(Ctrl)));
   CK(cudaMemsetAsync(h->row_idx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
-  CK(cudaMemsetAsync(h->col_idx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
   CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
 
   // Upload.  Offsets travel as int64 and are narrowed on the device.
@@ -420,7 +476,23 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   upload(h, h->cap, pv->capacities, 8 * static_cast<size_t>(m));
   CK(cudaStreamSynchronize(h->stream));
   cudaFree(off64);
-  build_csr(h, nullptr);
+
+  // Column blocks (stream ranges rounded to 32-stream tiles) and their CSRs.
+  const int nbk = choose_blocks(n);
+  CK(cudaMemsetAsync(h->deg, 0, sizeof(int) * static_cast<size_t>(m), h->stream));
+  for (int k = 0; k < nbk; ++k) {
+    ColBlock cb;
+    cb.s0 = (n * k / nbk) & ~31LL;
+    cb.s1 = (k + 1 == nbk) ? n : ((n * (k + 1) / nbk) & ~31LL);
+    const int64_t tb = pv->stream_offsets[cb.s0], te = pv->stream_offsets[cb.s1];
+    cb.nnz = te - tb;
+    cb.row_ptr = dalloc<int>(static_cast<size_t>(m) + 1, b);
+    cb.col_idx = dalloc<int>(static_cast<size_t>(cb.nnz) + kIdxPad, b);
+    h->blocks.push_back(cb);
+    build_csr(h, cb.s0, cb.s1, cb.row_ptr, cb.col_idx, nullptr);
+    k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
+    CK(cudaGetLastError());
+  }
 
   // Persistent grids: resident blocks x SMs.
   int sms = 0;
@@ -428,12 +500,16 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
-  const long long tiles1 = (n + 31) / 32, tiles2 = (m + 31) / 32;
+  int64_t max_bs = 0;
+  for (const ColBlock& cb : h->blocks) max_bs = std::max(max_bs, cb.s1 - cb.s0);
+  const long long tiles1 = (max_bs + 31) / 32, tiles2 = (m + 31) / 32;
   h->grid1 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ1, 1))));
   h->grid2 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ2, 1))));
-  h->k1_part = dalloc<double>(2 * static_cast<size_t>(std::max(h->grid1, h->grid2)), b);
+  h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
+                                  2 * static_cast<size_t>(std::max(h->grid2, h->grid1)),
+                              b);
   h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid2), b);
   h->trace_cap = h->cfg.max_iters / h->cfg.trace_every + 2;
   h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b);
@@ -485,8 +561,8 @@ void do_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rh
   const size_t nb = 8 * static_cast<size_t>(h->n), mb = 8 * static_cast<size_t>(h->m);
   upload(h, h->x, x0, nb);
   CK(cudaMemcpyAsync(h->A[0], h->x, nb, cudaMemcpyDeviceToDevice, h->stream));
-  global_row_sums(h, h->x, h->scratch_m);  // load = R x0, stream order per link
-  k_warm_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->deg, h->row_ptr, h->cap,
+  global_row_sums(h, h->x, h->scratch_m);  // load = R x0
+  k_warm_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->deg, nullptr, h->cap,
                                                        h->m, h->B[0], h->zs[0], h->Q[0], h->ps0,
                                                        h->pbar0);
   CK(cudaGetLastError());
@@ -551,7 +627,9 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
     h->nnz = pv->nnz;
     h->n_total = pv->n;
     h->nnz_total = pv->nnz;
-    if (world > 1) {
+    if (world >= 1 && nccl_id != nullptr) {
+      // Sharded handle (also with world == 1: the same kernels and the
+      // same all-reduce, over a one-rank communicator).
       h->sharded = true;
       h->rank = rank;
       h->world = world;
@@ -565,11 +643,8 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
     create_common(h, pv);
     if (h->sharded) {
       // Global link degrees and nnz: sums of the shards' local counts.
-      h->deg = dalloc<int>(static_cast<size_t>(h->m), &h->dev_bytes);
-      k_degree<<<grid_for(h->m), 256, 0, h->stream>>>(h->row_ptr, h->m, h->deg);
-      CK(cudaGetLastError());
       NK(AllReduce(h->deg, h->deg, static_cast<size_t>(h->m), ncclInt32, ncclSum, h->comm,
-                       h->stream));
+                   h->stream));
       double nnz_local = static_cast<double>(h->nnz);
       CK(cudaMemcpyAsync(h->scalars, &nnz_local, 8, cudaMemcpyHostToDevice, h->stream));
       NK(AllReduce(h->scalars, h->scalars, 1, ncclDouble, ncclSum, h->comm, h->stream));
@@ -604,7 +679,7 @@ int numpmp_gpu_create_sharded(const numpmp_problem_view* shard, const numpmp_con
                               int64_t stream_begin, int64_t n_total, numpmp_gpu** out) {
   if (world < 1 || rank < 0 || rank >= world)
     return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "bad rank/world");
-  if (world > 1 && !nccl_id) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "nccl_id is null");
+  if (!nccl_id) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "nccl_id is null");
   return create_impl(shard, config, device, rank, world, nccl_id, stream_begin, n_total, out);
 }
 
@@ -641,35 +716,35 @@ int numpmp_gpu_set_state(numpmp_gpu* h, const double* p, const double* z, const 
     if (!(rho > 0.0)) throw GpuError{NUMPMP_INVALID_ARGUMENT, "state rho must be > 0"};
     const int64_t n = h->n, m = h->m, nnz = h->nnz;
     std::vector<int> col_ptr(static_cast<size_t>(n) + 1), row_idx(static_cast<size_t>(nnz));
-    std::vector<int> row_ptr(static_cast<size_t>(m) + 1), col_idx(static_cast<size_t>(nnz));
     CK(cudaMemcpy(col_ptr.data(), h->col_ptr, 4 * (n + 1), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(row_idx.data(), h->row_idx, 4 * nnz, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(row_ptr.data(), h->row_ptr, 4 * (m + 1), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(col_idx.data(), h->col_idx, 4 * nnz, cudaMemcpyDeviceToHost));
-    // terminal of each CSR entry: position of link l in route j
+    // link -> (stream, terminal) adjacency on the host
+    std::vector<int64_t> loff(static_cast<size_t>(m) + 1, 0);
+    for (int64_t t = 0; t < nnz; ++t) ++loff[static_cast<size_t>(row_idx[static_cast<size_t>(t)]) + 1];
+    for (int64_t l = 0; l < m; ++l) loff[static_cast<size_t>(l) + 1] += loff[static_cast<size_t>(l)];
+    std::vector<int64_t> cursor(loff.begin(), loff.end() - 1), lterm(static_cast<size_t>(nnz));
+    for (int64_t t = 0; t < nnz; ++t) lterm[static_cast<size_t>(cursor[static_cast<size_t>(row_idx[static_cast<size_t>(t)])]++)] = t;
+    std::vector<int64_t> t2s(static_cast<size_t>(nnz));
+    for (int64_t j = 0; j < n; ++j)
+      for (int t = col_ptr[static_cast<size_t>(j)]; t < col_ptr[static_cast<size_t>(j) + 1]; ++t)
+        t2s[static_cast<size_t>(t)] = j;
     std::vector<double> A(static_cast<size_t>(n), 0.0), Bv(static_cast<size_t>(m), 0.0);
     std::vector<char> seen_s(static_cast<size_t>(n), 0), seen_l(static_cast<size_t>(m), 0);
-    std::vector<int64_t> queue;  // encoded: >= 0 link, < 0 stream (-(j+1))
-    auto term_of = [&](int64_t j, int l) -> int64_t {
-      for (int t = col_ptr[static_cast<size_t>(j)]; t < col_ptr[static_cast<size_t>(j) + 1]; ++t)
-        if (row_idx[static_cast<size_t>(t)] == l) return t;
-      return -1;
-    };
+    std::vector<int64_t> queue;  // >= 0 link, < 0 stream (-(j+1))
     for (int64_t root = 0; root < m; ++root) {
       if (seen_l[static_cast<size_t>(root)]) continue;
       seen_l[static_cast<size_t>(root)] = 1;
-      Bv[static_cast<size_t>(root)] = 0.0;
       queue.assign(1, root);
       for (size_t qi = 0; qi < queue.size(); ++qi) {
         const int64_t node = queue[qi];
         if (node >= 0) {
-          const int l = static_cast<int>(node);
-          for (int k = row_ptr[static_cast<size_t>(l)]; k < row_ptr[static_cast<size_t>(l) + 1]; ++k) {
-            const int j = col_idx[static_cast<size_t>(k)];
+          for (int64_t k = loff[static_cast<size_t>(node)]; k < loff[static_cast<size_t>(node) + 1]; ++k) {
+            const int64_t t = lterm[static_cast<size_t>(k)];
+            const int64_t j = t2s[static_cast<size_t>(t)];
             if (seen_s[static_cast<size_t>(j)]) continue;
             seen_s[static_cast<size_t>(j)] = 1;
-            A[static_cast<size_t>(j)] = z[term_of(j, l)] + Bv[static_cast<size_t>(l)];
-            queue.push_back(-(static_cast<int64_t>(j) + 1));
+            A[static_cast<size_t>(j)] = z[t] + Bv[static_cast<size_t>(node)];
+            queue.push_back(-(j + 1));
           }
         } else {
           const int64_t j = -node - 1;
@@ -685,7 +760,8 @@ int numpmp_gpu_set_state(numpmp_gpu* h, const double* p, const double* z, const 
     }
     for (int64_t j = 0; j < n; ++j)
       for (int t = col_ptr[static_cast<size_t>(j)]; t < col_ptr[static_cast<size_t>(j) + 1]; ++t) {
-        const double rec = A[static_cast<size_t>(j)] - Bv[static_cast<size_t>(row_idx[static_cast<size_t>(t)])];
+        const double rec =
+            A[static_cast<size_t>(j)] - Bv[static_cast<size_t>(row_idx[static_cast<size_t>(t)])];
         const double scale = std::max({1.0, std::fabs(z[t]), std::fabs(A[static_cast<size_t>(j)])});
         if (!(std::fabs(rec - z[t]) <= 1e-12 * scale))
           throw GpuError{NUMPMP_INVALID_ARGUMENT,
@@ -726,7 +802,7 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
       // slack flows and averages of the last iteration, same arithmetic
       global_row_sums(h, h->x, h->scratch_m);
       k_materialize_links<<<grid_for(m), 256, 0, h->stream>>>(
-          h->scratch_m, h->deg, h->row_ptr, h->cap, h->zs[pv], h->pr[pv], c.rho_iter, m,
+          h->scratch_m, h->deg, nullptr, h->cap, h->zs[pv], h->pr[pv], c.rho_iter, m,
           h->scratch_m2, h->Lbuf);
       CK(cudaGetLastError());
       ps_d = h->scratch_m2;
@@ -762,7 +838,7 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
 
 int numpmp_gpu_step(numpmp_gpu* h, double* r_norm, double* s_norm) {
   GUARD(h, {
-    enqueue_iteration(h, h->cur, MODE_STEP, nullptr, nullptr, nullptr);
+    enqueue_iteration(h, h->cur, MODE_STEP, nullptr, false);
     const Ctrl c = read_ctrl(h);
     h->cur ^= 1;
     h->iters_since_upload += 1;
@@ -780,10 +856,11 @@ namespace {
 // the device set `done` exit at entry.
 void run_loop(numpmp_gpu* h) {
   const int start = h->cur;
+  const int lpi = h->launches_per_iteration();
   cudaGraphExec_t exec;
   if (h->profiling) {
     if (h->prof_ev.empty()) {
-      h->prof_ev.resize(2 * kBatchIters + 1);
+      h->prof_ev.resize(static_cast<size_t>(kBatchIters * lpi + 1));
       for (auto& e : h->prof_ev) CK(cudaEventCreate(&e));
     }
     if (!h->prof_graph[start]) h->prof_graph[start] = build_graph(h, start, true);
@@ -821,18 +898,23 @@ void run_loop(numpmp_gpu* h) {
                        h->stream));
     CK(cudaEventRecord(h->ev_batch[slot], h->stream));
     ++inflight;
+    h->prof_launches += static_cast<int64_t>(kBatchIters) * lpi;
     if (h->profiling) {
       CK(cudaEventSynchronize(h->ev_batch[slot]));
       const Ctrl& c = h->ctrl_host[slot];
       const int64_t ran = c.run_k - k_seen;
       for (int64_t i = 0; i < ran && i < kBatchIters; ++i) {
-        float t1 = 0.f, t2 = 0.f;
-        CK(cudaEventElapsedTime(&t1, h->prof_ev[static_cast<size_t>(2 * i)],
-                                h->prof_ev[static_cast<size_t>(2 * i + 1)]));
-        CK(cudaEventElapsedTime(&t2, h->prof_ev[static_cast<size_t>(2 * i + 1)],
-                                h->prof_ev[static_cast<size_t>(2 * i + 2)]));
-        h->prof_ms_k1 += t1;
-        h->prof_ms_k2 += t2;
+        for (int l = 0; l < lpi; ++l) {
+          float t = 0.f;
+          const size_t e0 = static_cast<size_t>(i * lpi + l);
+          CK(cudaEventElapsedTime(&t, h->prof_ev[e0], h->prof_ev[e0 + 1]));
+          // launches alternate stream pass / link pass; the sharded
+          // epilogue (last launch) counts as link pass.
+          if ((l & 1) == 0 && l < 2 * h->nb())
+            h->prof_ms_k1 += t;
+          else
+            h->prof_ms_k2 += t;
+        }
         h->prof_iters += 1;
       }
       k_seen = c.run_k;
@@ -845,7 +927,6 @@ void run_loop(numpmp_gpu* h) {
       --inflight;
     }
     slot ^= 1;
-    h->prof_launches += kBatchIters * (h->sharded ? 3 : 2);
   }
   CK(cudaEventRecord(h->ev_run[1], h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -904,7 +985,8 @@ void post_process(numpmp_gpu* h, double* x, double* s, double* lambda, double* l
     ++tl;
   }
   if (trace)
-    std::memcpy(trace, rows.data(), sizeof(numpmp_trace_row) * static_cast<size_t>(std::min(tl, trace_cap)));
+    std::memcpy(trace, rows.data(),
+                sizeof(numpmp_trace_row) * static_cast<size_t>(std::min(tl, trace_cap)));
   if (info) {
     info->objective = obj[0];
     info->r_norm = c.r_norm;
@@ -948,11 +1030,22 @@ int numpmp_gpu_export_layout(numpmp_gpu* h, int64_t* link_offsets, int64_t* link
     if (h->sharded)
       throw GpuError{NUMPMP_INVALID_ARGUMENT, "export_layout is not supported on sharded handles"};
     const int64_t m = h->m, nnz = h->nnz;
+    // The global link-major CSR built on the device exactly as the column
+    // blocks are, plus the terminal ids the sort carried along.
+    int64_t tmpb = 0;
+    int* rp = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb);
+    int* ci = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
     std::vector<int> row_ptr(static_cast<size_t>(m) + 1), terms(static_cast<size_t>(nnz));
-    // Rebuild the sort to recover the terminal ids; the device CSR itself
-    // is checked against them (column = stream of terminal).
-    build_csr(h, terms.data());
-    CK(cudaMemcpy(row_ptr.data(), h->row_ptr, 4 * (m + 1), cudaMemcpyDeviceToHost));
+    try {
+      build_csr(h, 0, h->n, rp, ci, terms.data());
+      CK(cudaMemcpy(row_ptr.data(), rp, 4 * (m + 1), cudaMemcpyDeviceToHost));
+    } catch (...) {
+      cudaFree(rp);
+      cudaFree(ci);
+      throw;
+    }
+    cudaFree(rp);
+    cudaFree(ci);
     // model.hpp:182-199: |l| = degree + 1, slack terminal nnz + l last.
     link_offsets[0] = 0;
     for (int64_t l = 0; l < m; ++l) {
@@ -1030,6 +1123,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
     if (h->prof_graph[i]) cudaGraphExecDestroy(h->prof_graph[i]);
     if (h->ev_batch[i]) cudaEventDestroy(h->ev_batch[i]);
+    if (h->ev_run[i]) cudaEventDestroy(h->ev_run[i]);
     cudaFree(h->A[i]);
     cudaFree(h->B[i]);
     cudaFree(h->zs[i]);
@@ -1037,12 +1131,14 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     cudaFree(h->Q[i]);
   }
   for (auto& e : h->prof_ev) cudaEventDestroy(e);
-  for (auto& e : h->ev_run)
-    if (e) cudaEventDestroy(e);
-  void* bufs[] = {h->col_ptr, h->row_idx, h->w,        h->kind,     h->row_ptr,   h->col_idx,
-                  h->deg,     h->cap,     h->x,        h->v,        h->ps0,       h->pbar0,
-                  h->Lbuf,    h->k1_part, h->k2_part,  h->scratch_m, h->scratch_m2, h->scratch_n,
-                  h->scalars, h->ctrl,    h->trace_dev};
+  for (ColBlock& cb : h->blocks) {
+    cudaFree(cb.row_ptr);
+    cudaFree(cb.col_idx);
+  }
+  void* bufs[] = {h->col_ptr, h->row_idx,   h->w,         h->kind,      h->deg,      h->cap,
+                  h->x,       h->v,         h->ps0,       h->pbar0,     h->Lacc,     h->Lbuf,
+                  h->k1_part, h->k2_part,   h->scratch_m, h->scratch_m2, h->scratch_n, h->scalars,
+                  h->ctrl,    h->trace_dev};
   for (void* p : bufs) cudaFree(p);
   if (h->ctrl_host) cudaFreeHost(h->ctrl_host);
   if (h->comm) nccl().CommDestroy(h->comm);

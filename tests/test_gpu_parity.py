@@ -250,6 +250,46 @@ def test_solve_matches_oracle(case, restatement, oracle_mod):
     assert ok, err
 
 
+@pytest.mark.parametrize("blocks", [2, 3, 7])
+def test_column_blocks_match_oracle(blocks, restatement, oracle_mod, monkeypatch):
+    # the column-blocked pipeline (stream pass / link gather per block) is
+    # the same iteration: equal iteration counts, x and prices within 1e-6
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", str(blocks))
+    p = _gen(2000, 4000, 6.0, 2, True, 11)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+        st = s.final_state()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (st.p_bar, ref.final_pbar)]:
+        ok, err = close(got, want)
+        assert ok, err
+
+
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_sharded_path_one_rank_matches_oracle(blocks, restatement, oracle_mod, monkeypatch):
+    # The multi-GPU code path (local gather -> NCCL all-reduce of the partial
+    # loads + scalars -> replicated epilogue) on a one-rank communicator.
+    pytest.importorskip("torch")  # load PyTorch's NCCL first (shared with the engine)
+    from paper_2509_10722_b200.shard import ShardedPmpSolver, nccl_unique_id
+
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", str(blocks))
+    p = _gen(2000, 4000, 6.0, 2, True, 11)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    s = ShardedPmpSolver(p, cfg, 0, 1, nccl_unique_id())
+    try:
+        sol = s.solve()
+    finally:
+        s.close()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
+    assert abs(sol.objective - ref.objective) <= RTOL * abs(ref.objective)
+
+
 @pytest.mark.parametrize("K", [1, 10, 100])
 def test_step_state_matches_oracle(K, restatement, oracle_mod):
     # state-level parity of step() on config A

@@ -1,0 +1,140 @@
+"""CPU tests of the product's host side: the instance generator, degrade,
+validation and the reference layout (csrc/host_gen.cpp), each bit-exact
+against the reference (oracle/_ref) or the committed golden fixtures, and
+the multi-GPU shard partition."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2509_10722_b200 as pmp
+from paper_2509_10722_b200.shard import local_shard, shard_bounds
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _spec(m, n, avg, kind, weights, seed):
+    w = pmp.WeightDist.constant(weights[1]) if weights[0] == "constant" else pmp.WeightDist.uniform(weights[1], weights[2])
+    return pmp.GenSpec(m=m, n=n, avg_links_per_stream=avg, kind=pmp.GenKind(kind), weights=w, seed=seed)
+
+
+GEN_CASES = [
+    (1000, 10000, 5.0, 0, ("constant", 1.0, 1.0), 7),   # config A
+    (300, 150, 4.0, 2, ("uniform", 0.5, 1.5), 3),
+    (40, 20, 4.0, 2, ("constant", 1.0, 1.0), 9),
+    (200, 0, 10.0, 1, ("uniform", 0.0, 2.0), 5),          # n = 0 -> m/2, linear
+    (50, 30, 80.0, 0, ("constant", 2.0, 2.0), 1),         # routes capped at m
+]
+
+
+@pytest.mark.parametrize("case", GEN_CASES)
+def test_generator_bit_exact_with_reference(case, reference):
+    ra = reference.gen(*case).arrays()
+    p = pmp.gen_uncongested(_spec(*case))
+    assert (p.m, p.n, p.nnz) == (ra.m, ra.n, ra.nnz)
+    for mine, theirs in [(p.stream_offsets, ra.stream_offsets), (p.route_links, ra.route_links),
+                         (p.weights, ra.weights), (p.kinds, ra.kinds), (p.capacities, ra.capacities)]:
+        np.testing.assert_array_equal(mine, theirs)
+
+
+def test_config_b_nnz_matches_survey():
+    # config B has nnz 10,002,286
+    p = pmp.gen_uncongested(_spec(100000, 1000000, 10.0, 0, ("constant", 1.0, 1.0), 7))
+    assert p.nnz == 10002286
+
+
+def test_congested_generator_bit_exact(reference):
+    case = (400, 300, 4.0, 2, ("uniform", 0.5, 1.5), 13)
+    ra = reference.gen(*case, congested=True, hot_link_fraction=0.01, hot_stream_fraction=0.2).arrays()
+    p = pmp.gen_congested(_spec(*case), 0.01, 0.2)
+    np.testing.assert_array_equal(p.stream_offsets, ra.stream_offsets)
+    np.testing.assert_array_equal(p.route_links, ra.route_links)
+    np.testing.assert_array_equal(p.capacities, ra.capacities)
+
+
+def test_degrade_bit_exact(reference):
+    case = (500, 2000, 6.0, 2, ("uniform", 0.5, 1.5), 17)
+    rd = reference.gen(*case).degrade(0.5, 0.5, 99).arrays()
+    p = pmp.degrade(pmp.gen_uncongested(_spec(*case)), 0.5, 0.5, 99)
+    np.testing.assert_array_equal(p.capacities, rd.capacities)
+
+
+@pytest.mark.parametrize("name", ["config_a", "mixed_small", "transit_small"])
+def test_host_layout_matches_golden(name):
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    nnz = int(z["stream_offsets"][-1])
+    p = pmp.Problem(int(z["m"]), int(z["n"]), z["capacities"], z["weights"], z["kinds"], z["stream_offsets"],
+                    z["terminal_link"][:nnz])
+    L = p.layout
+    np.testing.assert_array_equal(L.terminal_link, z["terminal_link"])
+    np.testing.assert_array_equal(L.link_offsets, z["link_offsets"])
+    np.testing.assert_array_equal(L.link_terminals, z["link_terminals"])
+    np.testing.assert_array_equal(L.link_counts, z["link_counts"])
+    assert L.slack_terminal(3) == nnz + 3
+
+
+def test_bipartite_fixture_counts():
+    # test_model.cpp:19-31
+    S = pmp.Stream
+    p = pmp.build_problem([S(0, pmp.StreamKind.Log, "", 1.0, [0]), S(1, pmp.StreamKind.Log, "", 1.0, [1, 2]),
+                           S(2, pmp.StreamKind.Log, "", 1.0, [1])], [1.0, 1.0, 1.0])
+    assert (p.m, p.n, p.nnz, p.total_terminals) == (3, 3, 4, 7)
+    assert list(p.layout.link_counts) == [2, 3, 2]
+
+
+INVALID = [
+    # (routes, kinds, weights, caps) -- model.hpp:76-155 rules
+    ([[0, 0]], [0], [1.0], [1.0]),                 # distinct-links
+    ([[]], [0], [1.0], [1.0]),                     # non-empty-route
+    ([[3]], [0], [1.0], [1.0]),                    # link-in-range
+    ([[0]], [0], [1.0], [0.0, 1.0, 1.0]),          # positive-capacity
+    ([[0]], [0], [0.0], [1.0]),                    # positive-log-weight
+    ([[0]], [1], [-1.0], [1.0]),                   # nonnegative-weight
+    ([[0]], [0], [float("nan")], [1.0]),           # finite-weight
+    ([[0]], [0], [1.0], [float("inf")]),           # positive-capacity (non-finite)
+    ([[0, 0], [5], [1, 1]] * 4, [0] * 12, [1.0] * 12, [1.0, -1.0]),  # > 8 violations
+]
+
+
+@pytest.mark.parametrize("case", INVALID)
+def test_validation_messages_match_reference(case, reference):
+    routes, kinds, weights, caps = case
+    offs = np.cumsum([0] + [len(r) for r in routes]).astype(np.int64)
+    rl = np.array([x for r in routes for x in r], np.int32)
+    out = reference.build_problem(len(caps), len(routes), offs, rl, kinds, weights, caps)
+    assert isinstance(out, tuple) and out[0] == 2, out  # ValidationError
+    with pytest.raises(pmp.ValidationError) as ei:
+        pmp.problem_from_arrays(len(caps), len(routes), caps, weights, kinds, offs, rl)
+    assert str(ei.value) == out[1]
+
+
+def test_build_problem_rejects_empty():
+    with pytest.raises(pmp.ValidationError):
+        pmp.build_problem([], [1.0])
+    with pytest.raises(pmp.ValidationError):
+        pmp.build_problem([pmp.Stream(0, pmp.StreamKind.Log, "", 1.0, [0])], [])
+
+
+def test_generator_spec_errors():
+    with pytest.raises(pmp.GenError):
+        pmp.gen_uncongested(pmp.GenSpec(m=0))
+    with pytest.raises(pmp.GenError):
+        pmp.gen_uncongested(pmp.GenSpec(m=10, avg_links_per_stream=0.5))
+    with pytest.raises(pmp.GenError):
+        pmp.gen_uncongested(pmp.GenSpec(m=10, weights=pmp.WeightDist.uniform(2.0, 1.0)))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_bounds_tile_and_balance(world):
+    p = pmp.gen_uncongested(_spec(1000, 10000, 5.0, 2, ("uniform", 0.5, 1.5), 7))
+    b = shard_bounds(p.stream_offsets, world)
+    assert b[0] == 0 and b[-1] == p.n and np.all(np.diff(b) >= 0)
+    loads = np.diff(p.stream_offsets[b])
+    assert loads.sum() == p.nnz
+    assert loads.max() - loads.min() <= 2 * int(np.max(np.diff(p.stream_offsets)))  # within one stream's route
+    parts = [local_shard(p, r, world) for r in range(world)]
+    np.testing.assert_array_equal(np.concatenate([q.route_links for q, _ in parts]), p.route_links)
+    np.testing.assert_array_equal(np.concatenate([q.weights for q, _ in parts]), p.weights)
+    assert [s0 for _, s0 in parts] == list(b[:-1])
+    for q, _ in parts:
+        assert q.stream_offsets[0] == 0 and q.m == p.m

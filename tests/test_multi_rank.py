@@ -1,0 +1,143 @@
+"""World-size-2 CPU tests (gloo) of the multi-GPU decomposition.
+
+The sharded engine splits streams into contiguous, nnz-balanced ranges;
+each rank runs the stream pass on its shard, the ranks sum their partial
+link loads (plus two scalar partials) with one all-reduce, and every rank
+runs the identical replicated link update.  Here each rank executes that
+decomposed iteration in numpy (the same per-stream / per-link arithmetic as
+csrc/pmp_kernels.cuh) with torch.distributed over gloo as the all-reduce,
+and rank 0 checks the result against the CPU oracle after K iterations.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _prox(zeta, w, rho, tau, kind):
+    t = tau.astype(np.float64)
+    d = 4.0 * w * t / rho
+    root = np.sqrt(zeta * zeta + d)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        xl = np.where(zeta >= 0.0, (zeta + root) / (2.0 * t), d / (2.0 * t * (root - zeta)))
+    xlin = (zeta + w / rho) / t
+    xlin = np.where(xlin < 0.0, 0.0, xlin)
+    return np.where(kind == 0, xl, xlin)
+
+
+def _sharded_iterations(rank, world, p, cfg, K):
+    """K iterations of the decomposed PMP on this rank's shard."""
+    from paper_2509_10722_b200.shard import local_shard
+
+    q, s0 = local_shard(p, rank, world)
+    m = p.m
+    tau = np.diff(q.stream_offsets)
+    seg = np.repeat(np.arange(q.n), tau)
+    A = np.zeros(q.n)
+    B = np.zeros(m)
+    zs = np.zeros(m)
+    price = np.zeros(m)
+    Q = np.zeros(m)
+    rho = cfg["rho0"]
+    alpha = cfg["alpha"]
+    # global degree: all-reduce of the local counts
+    d_local = np.bincount(q.route_links, minlength=m).astype(np.float64)
+    t = torch.from_numpy(d_local)
+    dist.all_reduce(t)
+    deg = t.numpy()
+    rs = []
+    for _ in range(K):
+        v = B + price / rho
+        zeta = tau * A - np.bincount(seg, weights=v[q.route_links], minlength=q.n)
+        x = _prox(zeta, q.weights, rho, tau, q.kinds)
+        An = alpha * x + (1.0 - alpha) * A
+        dA = An - A
+        A = An
+        L_local = np.bincount(q.route_links, weights=x[seg], minlength=m)
+        buf = torch.from_numpy(np.concatenate([L_local, [np.sum(tau * dA * dA), 0.0]]))
+        dist.all_reduce(buf)  # the one exchange step of the iteration
+        L = buf.numpy()[:m]
+        tda2 = buf.numpy()[m]
+        # replicated link epilogue
+        ps = np.maximum(zs - price / rho, -p.capacities)
+        pbar = (L + ps) / (deg + 1.0)
+        r2 = np.sum((deg + 1.0) * pbar * pbar)
+        Bn = alpha * pbar + (1.0 - alpha) * B
+        zsn = alpha * (ps - pbar) + (1.0 - alpha) * zs
+        Qn = alpha * L + (1.0 - alpha) * Q
+        s2 = rho * rho * (tda2 - 2.0 * np.sum((Bn - B) * (Qn - Q)) + np.sum(deg * (Bn - B) ** 2)
+                          + np.sum((zsn - zs) ** 2))
+        price = price + rho * (alpha * pbar)
+        B, zs, Q = Bn, zsn, Qn
+        rs.append((np.sqrt(r2), np.sqrt(max(s2, 0.0))))
+    return s0, x, price, rs
+
+
+def _worker(rank, world, port, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2509_10722_b200 as pmp
+
+    p = pmp.gen_uncongested(pmp.GenSpec(m=300, n=900, avg_links_per_stream=5.0, kind=pmp.GenKind.Mixed,
+                                        weights=pmp.WeightDist.uniform(0.5, 1.5), seed=23))
+    cfg = dict(rho0=1.0, alpha=1.6)
+    s0, x, price, rs = _sharded_iterations(rank, world, p, cfg, 25)
+    # gather the x shards on rank 0
+    xs = [None] * world
+    dist.all_gather_object(xs, (s0, x))
+    # every rank holds the same replicated link state
+    t = torch.from_numpy(price.copy())
+    t0 = t.clone()
+    dist.broadcast(t0, 0)
+    same = bool(torch.equal(t, t0))
+    if rank == 0:
+        xfull = np.concatenate([xi for _, xi in sorted(xs, key=lambda a: a[0])])
+        result_q.put((xfull, price, rs, same))
+    else:
+        result_q.put(("ok", same))
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_iteration_matches_oracle(restatement, oracle_mod):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=300) for _ in range(2)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    main = [r for r in results if len(r) == 4][0]
+    other = [r for r in results if len(r) == 2][0]
+    xfull, price, rs, same0 = main
+    assert same0 and other[1], "replicated link state diverged across ranks"
+
+    import paper_2509_10722_b200 as pmp
+
+    p = pmp.gen_uncongested(pmp.GenSpec(m=300, n=900, avg_links_per_stream=5.0, kind=pmp.GenKind.Mixed,
+                                        weights=pmp.WeightDist.uniform(0.5, 1.5), seed=23))
+    a = oracle_mod.arrays_from(p)
+    cfg = oracle_mod.Config(rho0=1.0, alpha=1.6, rho_update_interval=10 ** 6)
+    st = restatement.cold_state(a, cfg)
+    for k in range(25):
+        r, s, x = restatement.step(a, cfg, st)
+        assert abs(rs[k][0] - r) <= 1e-9 * max(r, 1e-300)
+        assert abs(rs[k][1] - s) <= 1e-7 * max(s, 1e-300)
+    np.testing.assert_allclose(xfull, x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(price, st["price"], rtol=1e-9, atol=1e-12)
