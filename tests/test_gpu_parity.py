@@ -422,6 +422,21 @@ def test_config_validation():
             pmp.PmpSolver(p, pmp.SolverConfig(**bad))
 
 
+def test_cpp_dropin_binary():
+    # include/numpmp/gpu_solver.hpp against the reference's own CPU
+    # PmpSolver in one C++ binary (tests/cpp/test_dropin.cpp)
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("build/test_dropin not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ALL PASSED" in out.stdout
+
+
 # ------------------------------------------------------------- config B / C
 @pytest.mark.slow
 def test_config_b_iterations_match_oracle(restatement, oracle_mod):
