@@ -6,6 +6,45 @@
 
 namespace numpmp_dev {
 
+// Model validation on the device (the rules of model.hpp:76-135): one
+// counter per rule; any nonzero count sends the caller to the host
+// validator, which produces the reference's exact message.
+//   bad[0] capacity, bad[1] empty route / offsets, bad[2] link out of range,
+//   bad[3] duplicate link, bad[4] weight, bad[5] kind
+__global__ void k_validate(const long long* __restrict__ off, const int* __restrict__ links,
+                           const double* __restrict__ w, const unsigned char* __restrict__ kind,
+                           const double* __restrict__ cap, long long n, long long m,
+                           unsigned long long* __restrict__ bad) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  for (long long l = tid; l < m; l += stride) {
+    const double v = cap[l];
+    if (!(v > 0.0) || !isfinite(v)) ++c[0];
+  }
+  for (long long j = tid; j < n; j += stride) {
+    const long long b = off[j], e = off[j + 1];
+    if (e <= b) ++c[1];
+    for (long long t = b; t < e; ++t) {
+      const int l = links[t];
+      if (l < 0 || l >= m) ++c[2];
+      for (long long u = b; u < t; ++u)
+        if (links[u] == l) {
+          ++c[3];
+          break;
+        }
+    }
+    const double wj = w[j];
+    const int k = kind[j];
+    if (!isfinite(wj) || (k == NUMPMP_KIND_LOG && !(wj > 0.0)) || (k != NUMPMP_KIND_LOG && wj < 0.0))
+      ++c[4];
+    if (k >= NUMPMP_KIND_EXTENSION) ++c[5];  // extension (or unknown) utility
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+    if (c[i]) atomicAdd(bad + i, c[i]);
+}
+
 // int64 stream offsets -> int32 CSC column pointer (nnz < 2^31 checked on host).
 __global__ void k_offsets_to_i32(const long long* __restrict__ in, int* __restrict__ out,
                                  long long count) {

@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -104,6 +105,20 @@ int grid_for(long long work, int threads = 256) {
   if (b > 148 * 32) b = 148 * 32;
   return static_cast<int>(b);
 }
+
+// NUMPMP_TIMING=1: host wall time of the setup / run / teardown phases on
+// stderr (end-to-end accounting of the C-ABI calls).
+struct PhaseTimer {
+  bool on = std::getenv("NUMPMP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[numpmp] %-28s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // One column block of the device problem (see pmp_kernels.cuh).
 struct ColBlock {
@@ -432,8 +447,10 @@ int choose_blocks(int64_t n) {
 }
 
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
+  PhaseTimer pt;
   CK(cudaSetDevice(h->device));
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  pt.mark("create: stream");
   const int64_t m = h->m, n = h->n, nnz = h->nnz;
   int64_t* b = &h->dev_bytes;
   h->col_ptr = dalloc<int>(static_cast<size_t>(n) + 1, b);
@@ -474,8 +491,36 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   upload(h, h->w, pv->weights, 8 * static_cast<size_t>(n));
   upload(h, h->kind, pv->kinds, static_cast<size_t>(n));
   upload(h, h->cap, pv->capacities, 8 * static_cast<size_t>(m));
-  CK(cudaStreamSynchronize(h->stream));
-  cudaFree(off64);
+  pt.mark("create: alloc + upload");
+
+  // Model validation (model.hpp:76-155) on the device; only an invalid
+  // problem pays for the host validator, which words the reference's exact
+  // ValidationError message.  Extension streams: SolverError
+  // (solver.hpp:275-284; no device prox).
+  {
+    unsigned long long* bad = nullptr;
+    CK(cudaMalloc(&bad, 6 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(bad, 0, 6 * sizeof(unsigned long long), h->stream));
+    k_validate<<<grid_for(std::max(n, m)), 256, 0, h->stream>>>(off64, h->row_idx, h->w, h->kind,
+                                                               h->cap, n, m, bad);
+    CK(cudaGetLastError());
+    unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(cnt, bad, sizeof(cnt), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(bad);
+    cudaFree(off64);
+    if (cnt[0] + cnt[1] + cnt[2] + cnt[3] + cnt[4] > 0) {
+      std::vector<char> msg(4096);
+      numpmp_validate(pv->m, pv->n, pv->capacities, pv->weights, pv->kinds, pv->stream_offsets,
+                      pv->route_links, msg.data(), static_cast<int64_t>(msg.size()));
+      throw GpuError{NUMPMP_VALIDATION_ERROR, msg.data()};
+    }
+    if (cnt[5] > 0)
+      throw GpuError{NUMPMP_SOLVER_ERROR,
+                     "no extension registered for utility (extension utilities are host "
+                     "callbacks and are not supported by the device engine)"};
+  }
+  pt.mark("create: device validation");
 
   // Column blocks (stream ranges rounded to 32-stream tiles) and their CSRs.
   const int nbk = choose_blocks(n);
@@ -493,6 +538,8 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
     CK(cudaGetLastError());
   }
+  CK(cudaStreamSynchronize(h->stream));
+  pt.mark("create: device CSR build");
 
   // Persistent grids: resident blocks x SMs.
   int sms = 0;
@@ -515,6 +562,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b);
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&h->ev_batch[i], cudaEventDisableTiming));
   CK(cudaStreamSynchronize(h->stream));
+  pt.mark("create: grids + buffers");
 }
 
 void reset_ctrl(numpmp_gpu* h, double rho, int64_t iter) {
@@ -603,22 +651,9 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
   if (!cfg) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "config is null");
   if (const char* msg = validate_config(cfg)) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, msg);
   numpmp_gpu* h = nullptr;
+  PhaseTimer pt;
   try {
     check_view(pv);
-    // model.hpp:76-155 on the host view (same rules and messages).
-    {
-      std::vector<char> msg(4096);
-      const int64_t nv = numpmp_validate(pv->m, pv->n, pv->capacities, pv->weights, pv->kinds,
-                                         pv->stream_offsets, pv->route_links, msg.data(),
-                                         static_cast<int64_t>(msg.size()));
-      if (nv > 0) throw GpuError{NUMPMP_VALIDATION_ERROR, msg.data()};
-    }
-    // solver.hpp:275-284: extension utilities have no device prox.
-    for (int64_t j = 0; j < pv->n; ++j)
-      if (pv->kinds[j] == NUMPMP_KIND_EXTENSION)
-        throw GpuError{NUMPMP_SOLVER_ERROR,
-                       "no extension registered for utility (extension utilities are host "
-                       "callbacks and are not supported by the device engine)"};
     h = new numpmp_gpu();
     h->cfg = *cfg;
     h->device = device;
@@ -654,6 +689,7 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
       h->nnz_total = static_cast<int64_t>(nnz_global);
     }
     do_set_cold(h);
+    pt.mark("create: total after validation");
     h->h2d = 0;
     h->d2h = 0;
     *out = h;
@@ -855,6 +891,7 @@ namespace {
 // queued, so the device never idles on the host.  Kernels queued after
 // the device set `done` exit at entry.
 void run_loop(numpmp_gpu* h) {
+  PhaseTimer pt;
   const int start = h->cur;
   const int lpi = h->launches_per_iteration();
   cudaGraphExec_t exec;
@@ -887,6 +924,7 @@ void run_loop(numpmp_gpu* h) {
     CK(cudaEventCreate(&h->ev_run[1]));
   }
   CK(cudaEventRecord(h->ev_run[0], h->stream));
+  pt.mark("run: graph + control reset");
   k_start_clock<<<1, 1, 0, h->stream>>>(h->ctrl);
   CK(cudaGetLastError());
   int64_t k_seen = 0;
@@ -936,6 +974,7 @@ void run_loop(numpmp_gpu* h) {
     CK(cudaEventElapsedTime(&ms, h->ev_run[0], h->ev_run[1]));
     h->last_run_ms = ms;
   }
+  pt.mark("run: iteration loop");
   h->run_iters = c.run_k;
   h->iters_since_upload += c.run_k;
   h->cur = static_cast<int>((start + c.run_k) & 1);
@@ -950,6 +989,7 @@ void run_loop(numpmp_gpu* h) {
 // Solution post-processing (solver.hpp:478-504) on the device.
 void post_process(numpmp_gpu* h, double* x, double* s, double* lambda, double* lambda_raw,
                   numpmp_solution_info* info, numpmp_trace_row* trace, int64_t trace_cap) {
+  PhaseTimer pt;
   const Ctrl c = read_ctrl(h);
   const int cu = h->cur;
   const int gpost = std::min(grid_for(h->n), h->grid1);
@@ -984,6 +1024,7 @@ void post_process(numpmp_gpu* h, double* x, double* s, double* lambda, double* l
     r.objective = obj[1];
     ++tl;
   }
+  pt.mark("post-process + download");
   if (trace)
     std::memcpy(trace, rows.data(),
                 sizeof(numpmp_trace_row) * static_cast<size_t>(std::min(tl, trace_cap)));
@@ -1117,6 +1158,7 @@ int numpmp_gpu_transfer_bytes(const numpmp_gpu* h, int64_t* h2d, int64_t* d2h) {
 
 void numpmp_gpu_destroy(numpmp_gpu* h) {
   if (!h) return;
+  PhaseTimer pt;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (int i = 0; i < 2; ++i) {
@@ -1144,6 +1186,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
+  pt.mark("destroy");
 }
 
 }  // extern "C"

@@ -78,22 +78,14 @@ def test_config_errors_are_invalid_argument(bad, msg):
     assert not h.value
 
 
-def test_invalid_problem_is_validation_error():
+def test_malformed_view_is_rejected_on_host():
     L = _lib.lib()
-    p = pmp.Problem(1, 1, [0.0], [1.0], [0], [0, 1], [0])  # capacity 0
+    p = pmp.Problem(1, 1, [1.0], [1.0], [0], [0, 2], [0, 0])
     view = p.view()
+    view.nnz = 1  # offsets say 2 terminals
     h = C.c_void_p()
-    rc = L.numpmp_gpu_create(C.byref(view), C.byref(_cfg()), 0, C.byref(h))
-    assert rc == 2
-    assert "positive-capacity" in L.numpmp_gpu_last_error(None).decode()
-
-
-def test_extension_stream_is_solver_error():
-    L = _lib.lib()
-    p = pmp.Problem(1, 1, [1.0], [1.0], [2], [0, 1], [0])
-    view = p.view()
-    h = C.c_void_p()
-    assert L.numpmp_gpu_create(C.byref(view), C.byref(_cfg()), 0, C.byref(h)) == 3
+    assert L.numpmp_gpu_create(C.byref(view), C.byref(_cfg()), 0, C.byref(h)) == 2
+    assert "incidence-nnz" in L.numpmp_gpu_last_error(None).decode()
 
 
 def test_null_handle_calls_fail_cleanly():

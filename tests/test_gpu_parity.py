@@ -413,6 +413,31 @@ def test_extension_streams_rejected():
         pmp.PmpSolver(p)
 
 
+INVALID = [
+    # (routes, kinds, weights, caps): model.hpp:76-155 rules, detected on the device
+    ([[0, 0]], [0], [1.0], [1.0]),
+    ([[]], [0], [1.0], [1.0]),
+    ([[3]], [0], [1.0], [1.0]),
+    ([[0]], [0], [1.0], [0.0, 1.0, 1.0]),
+    ([[0]], [0], [0.0], [1.0]),
+    ([[0]], [1], [-1.0], [1.0]),
+    ([[0]], [0], [float("nan")], [1.0]),
+    ([[0, 0], [5], [1, 1]] * 4, [0] * 12, [1.0] * 12, [1.0, -1.0]),
+]
+
+
+@pytest.mark.parametrize("case", INVALID)
+def test_device_validation_raises_reference_message(case, reference):
+    routes, kinds, weights, caps = case
+    offs = np.cumsum([0] + [len(r) for r in routes]).astype(np.int64)
+    rl = np.array([x for r in routes for x in r], np.int32)
+    out = reference.build_problem(len(caps), len(routes), offs, rl, kinds, weights, caps)
+    p = pmp.Problem(len(caps), len(routes), caps, weights, kinds, offs, rl)  # unvalidated
+    with pytest.raises(pmp.ValidationError) as ei:
+        pmp.PmpSolver(p)
+    assert str(ei.value) == out[1]
+
+
 def test_config_validation():
     p = single()
     for bad in [dict(eps_abs=0.0), dict(rho0=-1.0), dict(alpha=2.5), dict(mu=1.0), dict(gamma=1.0),
