@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libnumpmp_cuda.so")
+# NUMPMP_LIB selects an alternative in-tree build (tuning sweeps, scripts/variants.sh)
+LIB_PATH = os.environ.get("NUMPMP_LIB") or os.path.join(_HERE, "lib", "libnumpmp_cuda.so")
 
 
 class ProblemView(C.Structure):

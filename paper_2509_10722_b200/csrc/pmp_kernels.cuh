@@ -43,10 +43,24 @@
 
 namespace numpmp_dev {
 
-constexpr int kWarps = 8;  // warps per block (gather passes)
+// Tuning knobs (overridable at build time for sweeps, scripts/variants.sh).
+#ifndef NUMPMP_WARPS
+#define NUMPMP_WARPS 8
+#endif
+#ifndef NUMPMP_MIN_BLOCKS
+#define NUMPMP_MIN_BLOCKS 4
+#endif
+#ifndef NUMPMP_STAGE_INTS
+#define NUMPMP_STAGE_INTS 512
+#endif
+#ifndef NUMPMP_GATHER_UNROLL
+#define NUMPMP_GATHER_UNROLL 4
+#endif
+constexpr int kWarps = NUMPMP_WARPS;  // warps per block (gather passes)
 constexpr int kThreads = kWarps * 32;
-constexpr int kMinBlocks = 4;  // resident blocks per SM the gather passes are built for (<= 64 regs)
-constexpr int kStageInts = 512;  // staged indices per warp and round (2 KB)
+constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
+constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
+constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { ST_RUNNING = -1, ST_CONVERGED = 0, ST_MAXITERS = 1, ST_TIMELIMIT = 2,
@@ -233,14 +247,15 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
     }
     const int lo = max(seg_beg, cb), hi = min(seg_end, c1);
     int k = lo;
-    for (; k + 4 <= hi; k += 4) {
-      const int i0 = sidx[k - cb], i1 = sidx[k + 1 - cb], i2 = sidx[k + 2 - cb],
-                i3 = sidx[k + 3 - cb];
-      const double v0 = g(i0), v1 = g(i1), v2 = g(i2), v3 = g(i3);
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
+    for (; k + kUnroll <= hi; k += kUnroll) {
+      int ii[kUnroll];
+      double vv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) ii[u] = sidx[k + u - cb];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) vv[u] = g(ii[u]);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc += vv[u];
     }
     for (; k < hi; ++k) acc += g(sidx[k - cb]);
     __syncwarp();
