@@ -90,11 +90,25 @@ const NcclApi& nccl() {
 
 thread_local std::string g_create_err;
 
+// Device memory comes from the device's stream-ordered pool, which is told
+// to keep freed memory reserved: creating and destroying solver handles
+// (e2e steps, warm re-solves) then costs no cudaMalloc/cudaFree round trips.
+void keep_pool_memory(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 template <class T>
-T* dalloc(size_t count, int64_t* bytes) {
+T* dalloc(size_t count, int64_t* bytes, cudaStream_t stream) {
   T* p = nullptr;
   const size_t b = sizeof(T) * (count > 0 ? count : 1);
-  CK(cudaMalloc(&p, b));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&p), b, stream));
   *bytes += static_cast<int64_t>(b);
   return p;
 }
@@ -182,10 +196,10 @@ struct numpmp_gpu {
   int last_status = NUMPMP_MAXITERS;
 
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
-  cudaGraphExec_t prof_graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t prof_graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [parity][set]
   cudaEvent_t ev_batch[2] = {nullptr, nullptr};
   bool profiling = false;
-  std::vector<cudaEvent_t> prof_ev;  // 1 + kBatchIters * launches_per_iteration
+  std::vector<cudaEvent_t> prof_ev;  // 2 sets of 1 + kBatchIters * launches_per_iteration
   int64_t prof_launches = 0, prof_iters = 0;
   double prof_ms_k1 = 0.0, prof_ms_k2 = 0.0;
 
@@ -318,14 +332,18 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
   }
 }
 
-cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, bool with_events) {
+// ev_set < 0: no events; else the graph records event set ev_set
+// (1 + kBatchIters * launches_per_iteration events) around every launch.
+cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
   cudaGraph_t g = nullptr;
   const int lpi = h->launches_per_iteration();
+  const size_t set_base = ev_set < 0 ? 0 : static_cast<size_t>(ev_set) * (kBatchIters * lpi + 1);
   CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   try {
     for (int i = 0; i < kBatchIters; ++i)
       enqueue_iteration(h, parity ^ (i & 1), MODE_RUN,
-                        with_events ? &h->prof_ev[static_cast<size_t>(i * lpi)] : nullptr, i == 0);
+                        ev_set >= 0 ? &h->prof_ev[set_base + static_cast<size_t>(i * lpi)] : nullptr,
+                        i == 0);
   } catch (...) {
     cudaStreamEndCapture(h->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -378,17 +396,17 @@ void build_csr(numpmp_gpu* h, int64_t s0, int64_t s1, int* row_ptr_out, int* col
   CK(cudaMemcpy(&bounds[1], h->col_ptr + s1, 4, cudaMemcpyDeviceToHost));
   const long long t0 = bounds[0], nnz = bounds[1] - bounds[0], ns = s1 - s0;
   int64_t tmpb = 0;
-  int* keys_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
-  int* vals_in = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
-  int* vals_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
-  int* t2s = dalloc<int>(static_cast<size_t>(h->nnz) + kIdxPad, &tmpb);
+  int* keys_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb, h->stream);
+  int* vals_in = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb, h->stream);
+  int* vals_out = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb, h->stream);
+  int* t2s = dalloc<int>(static_cast<size_t>(h->nnz) + kIdxPad, &tmpb, h->stream);
   void* temp = nullptr;
   auto release = [&]() {
-    cudaFree(temp);
-    cudaFree(keys_out);
-    cudaFree(vals_in);
-    cudaFree(vals_out);
-    cudaFree(t2s);
+    cudaFreeAsync(temp, h->stream);
+    cudaFreeAsync(keys_out, h->stream);
+    cudaFreeAsync(vals_in, h->stream);
+    cudaFreeAsync(vals_out, h->stream);
+    cudaFreeAsync(t2s, h->stream);
   };
   try {
     k_iota<<<grid_for(nnz), 256, 0, h->stream>>>(vals_in, nnz, t0);
@@ -399,7 +417,7 @@ void build_csr(numpmp_gpu* h, int64_t s0, int64_t s1, int* row_ptr_out, int* col
     size_t temp_bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, h->row_idx + t0, keys_out, vals_in,
                                        vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
-    CK(cudaMalloc(&temp, temp_bytes > 0 ? temp_bytes : 1));
+    CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
     CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, h->row_idx + t0, keys_out, vals_in,
                                        vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
     k_row_ptr_from_sorted<<<grid_for(nnz + 1), 256, 0, h->stream>>>(keys_out, nnz, h->m,
@@ -449,41 +467,42 @@ int choose_blocks(int64_t n) {
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   PhaseTimer pt;
   CK(cudaSetDevice(h->device));
+  keep_pool_memory(h->device);
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   pt.mark("create: stream");
   const int64_t m = h->m, n = h->n, nnz = h->nnz;
   int64_t* b = &h->dev_bytes;
-  h->col_ptr = dalloc<int>(static_cast<size_t>(n) + 1, b);
-  h->row_idx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, b);
-  h->w = dalloc<double>(static_cast<size_t>(n), b);
-  h->kind = dalloc<unsigned char>(static_cast<size_t>(n), b);
-  h->cap = dalloc<double>(static_cast<size_t>(m), b);
-  h->deg = dalloc<int>(static_cast<size_t>(m), b);
+  h->col_ptr = dalloc<int>(static_cast<size_t>(n) + 1, b, h->stream);
+  h->row_idx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, b, h->stream);
+  h->w = dalloc<double>(static_cast<size_t>(n), b, h->stream);
+  h->kind = dalloc<unsigned char>(static_cast<size_t>(n), b, h->stream);
+  h->cap = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->deg = dalloc<int>(static_cast<size_t>(m), b, h->stream);
   for (int i = 0; i < 2; ++i) {
-    h->A[i] = dalloc<double>(static_cast<size_t>(n), b);
-    h->B[i] = dalloc<double>(static_cast<size_t>(m), b);
-    h->zs[i] = dalloc<double>(static_cast<size_t>(m), b);
-    h->pr[i] = dalloc<double>(static_cast<size_t>(m), b);
-    h->Q[i] = dalloc<double>(static_cast<size_t>(m), b);
+    h->A[i] = dalloc<double>(static_cast<size_t>(n), b, h->stream);
+    h->B[i] = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+    h->zs[i] = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+    h->pr[i] = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+    h->Q[i] = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   }
-  h->x = dalloc<double>(static_cast<size_t>(n), b);
-  h->v = dalloc<double>(static_cast<size_t>(m), b);
-  h->ps0 = dalloc<double>(static_cast<size_t>(m), b);
-  h->pbar0 = dalloc<double>(static_cast<size_t>(m), b);
-  h->Lacc = dalloc<double>(static_cast<size_t>(m), b);
-  h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b);
-  h->scratch_m = dalloc<double>(static_cast<size_t>(m), b);
-  h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b);
-  h->scratch_n = dalloc<double>(static_cast<size_t>(n), b);
-  h->scalars = dalloc<double>(2, b);
-  h->ctrl = dalloc<Ctrl>(1, b);
+  h->x = dalloc<double>(static_cast<size_t>(n), b, h->stream);
+  h->v = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->ps0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->pbar0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->Lacc = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b, h->stream);
+  h->scratch_m = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  h->scratch_n = dalloc<double>(static_cast<size_t>(n), b, h->stream);
+  h->scalars = dalloc<double>(2, b, h->stream);
+  h->ctrl = dalloc<Ctrl>(1, b, h->stream);
   CK(cudaMallocHost(&h->ctrl_host, 2 * sizeof(Ctrl)));
   CK(cudaMemsetAsync(h->row_idx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
   CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
 
   // Upload.  Offsets travel as int64 and are narrowed on the device.
   long long* off64 = nullptr;
-  CK(cudaMalloc(&off64, 8 * static_cast<size_t>(n + 1)));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&off64), 8 * static_cast<size_t>(n + 1), h->stream));
   upload(h, off64, pv->stream_offsets, 8 * static_cast<size_t>(n + 1));
   k_offsets_to_i32<<<grid_for(n + 1), 256, 0, h->stream>>>(off64, h->col_ptr, n + 1);
   CK(cudaGetLastError());
@@ -499,7 +518,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   // (solver.hpp:275-284; no device prox).
   {
     unsigned long long* bad = nullptr;
-    CK(cudaMalloc(&bad, 6 * sizeof(unsigned long long)));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&bad), 6 * sizeof(unsigned long long), h->stream));
     CK(cudaMemsetAsync(bad, 0, 6 * sizeof(unsigned long long), h->stream));
     k_validate<<<grid_for(std::max(n, m)), 256, 0, h->stream>>>(off64, h->row_idx, h->w, h->kind,
                                                                h->cap, n, m, bad);
@@ -507,8 +526,8 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(cnt, bad, sizeof(cnt), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    cudaFree(bad);
-    cudaFree(off64);
+    cudaFreeAsync(bad, h->stream);
+    cudaFreeAsync(off64, h->stream);
     if (cnt[0] + cnt[1] + cnt[2] + cnt[3] + cnt[4] > 0) {
       std::vector<char> msg(4096);
       numpmp_validate(pv->m, pv->n, pv->capacities, pv->weights, pv->kinds, pv->stream_offsets,
@@ -531,8 +550,8 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     cb.s1 = (k + 1 == nbk) ? n : ((n * (k + 1) / nbk) & ~31LL);
     const int64_t tb = pv->stream_offsets[cb.s0], te = pv->stream_offsets[cb.s1];
     cb.nnz = te - tb;
-    cb.row_ptr = dalloc<int>(static_cast<size_t>(m) + 1, b);
-    cb.col_idx = dalloc<int>(static_cast<size_t>(cb.nnz) + kIdxPad, b);
+    cb.row_ptr = dalloc<int>(static_cast<size_t>(m) + 1, b, h->stream);
+    cb.col_idx = dalloc<int>(static_cast<size_t>(cb.nnz) + kIdxPad, b, h->stream);
     h->blocks.push_back(cb);
     build_csr(h, cb.s0, cb.s1, cb.row_ptr, cb.col_idx, nullptr);
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
@@ -556,10 +575,10 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
       1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ2, 1))));
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
                                   2 * static_cast<size_t>(std::max(h->grid2, h->grid1)),
-                              b);
-  h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid2), b);
+                              b, h->stream);
+  h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid2), b, h->stream);
   h->trace_cap = h->cfg.max_iters / h->cfg.trace_every + 2;
-  h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b);
+  h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b, h->stream);
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&h->ev_batch[i], cudaEventDisableTiming));
   CK(cudaStreamSynchronize(h->stream));
   pt.mark("create: grids + buffers");
@@ -847,9 +866,9 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
     const size_t J = static_cast<size_t>(nnz + m);
     double *dp = nullptr, *dz = nullptr, *dzp = nullptr;
     if (p || z || prev_z) {
-      if (p) CK(cudaMalloc(&dp, 8 * J));
-      if (z) CK(cudaMalloc(&dz, 8 * J));
-      if (prev_z) CK(cudaMalloc(&dzp, 8 * J));
+      if (p) CK(cudaMallocAsync(reinterpret_cast<void**>(&dp), 8 * J, h->stream));
+      if (z) CK(cudaMallocAsync(reinterpret_cast<void**>(&dz), 8 * J, h->stream));
+      if (prev_z) CK(cudaMallocAsync(reinterpret_cast<void**>(&dzp), 8 * J, h->stream));
       k_expand_terminals<<<grid_for(n), 256, 0, h->stream>>>(
           h->col_ptr, h->row_idx, n, h->x, h->A[cu], h->B[cu], h->A[pv], h->B[pv], dp, dz, dzp);
       CK(cudaGetLastError());
@@ -862,9 +881,9 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
     }
     if (p_bar) download(h, p_bar, pbar_d, 8 * static_cast<size_t>(m));
     CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dp);
-    cudaFree(dz);
-    cudaFree(dzp);
+    cudaFreeAsync(dp, h->stream);
+    cudaFreeAsync(dz, h->stream);
+    cudaFreeAsync(dzp, h->stream);
     if (!stepped && h->host_p_valid) {
       if (p) std::memcpy(p, h->host_p.data(), 8 * J);
       if (p_bar) std::memcpy(p_bar, h->host_pbar.data(), 8 * static_cast<size_t>(m));
@@ -894,17 +913,16 @@ void run_loop(numpmp_gpu* h) {
   PhaseTimer pt;
   const int start = h->cur;
   const int lpi = h->launches_per_iteration();
-  cudaGraphExec_t exec;
+  const size_t set_size = static_cast<size_t>(kBatchIters * lpi + 1);
   if (h->profiling) {
     if (h->prof_ev.empty()) {
-      h->prof_ev.resize(static_cast<size_t>(kBatchIters * lpi + 1));
+      h->prof_ev.resize(2 * set_size);
       for (auto& e : h->prof_ev) CK(cudaEventCreate(&e));
     }
-    if (!h->prof_graph[start]) h->prof_graph[start] = build_graph(h, start, true);
-    exec = h->prof_graph[start];
-  } else {
-    if (!h->graph[start]) h->graph[start] = build_graph(h, start, false);
-    exec = h->graph[start];
+    for (int set = 0; set < 2; ++set)
+      if (!h->prof_graph[start][set]) h->prof_graph[start][set] = build_graph(h, start, set);
+  } else if (!h->graph[start]) {
+    h->graph[start] = build_graph(h, start, -1);
   }
   // fresh run: control counters, trace, device clock
   {
@@ -927,44 +945,48 @@ void run_loop(numpmp_gpu* h) {
   pt.mark("run: graph + control reset");
   k_start_clock<<<1, 1, 0, h->stream>>>(h->ctrl);
   CK(cudaGetLastError());
+  // Per-kernel event times of a finished batch (profiling mode): only the
+  // iterations that batch actually ran count.
   int64_t k_seen = 0;
+  auto account = [&](int set, const Ctrl& c) {
+    const int64_t ran = c.run_k - k_seen;
+    for (int64_t i = 0; i < ran && i < kBatchIters; ++i) {
+      for (int l = 0; l < lpi; ++l) {
+        float t = 0.f;
+        const size_t e0 = static_cast<size_t>(set) * set_size + static_cast<size_t>(i * lpi + l);
+        CK(cudaEventElapsedTime(&t, h->prof_ev[e0], h->prof_ev[e0 + 1]));
+        // launches alternate stream pass / link pass; the sharded
+        // epilogue (last launch) counts as link pass.
+        if ((l & 1) == 0 && l < 2 * h->nb())
+          h->prof_ms_k1 += t;
+        else
+          h->prof_ms_k2 += t;
+      }
+      h->prof_iters += 1;
+    }
+    k_seen = c.run_k;
+  };
   int inflight = 0, slot = 0;
   bool done = false;
   while (!done) {
-    CK(cudaGraphLaunch(exec, h->stream));
+    CK(cudaGraphLaunch(h->profiling ? h->prof_graph[start][slot] : h->graph[start], h->stream));
     CK(cudaMemcpyAsync(h->ctrl_host + slot, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
                        h->stream));
     CK(cudaEventRecord(h->ev_batch[slot], h->stream));
     ++inflight;
     h->prof_launches += static_cast<int64_t>(kBatchIters) * lpi;
-    if (h->profiling) {
-      CK(cudaEventSynchronize(h->ev_batch[slot]));
-      const Ctrl& c = h->ctrl_host[slot];
-      const int64_t ran = c.run_k - k_seen;
-      for (int64_t i = 0; i < ran && i < kBatchIters; ++i) {
-        for (int l = 0; l < lpi; ++l) {
-          float t = 0.f;
-          const size_t e0 = static_cast<size_t>(i * lpi + l);
-          CK(cudaEventElapsedTime(&t, h->prof_ev[e0], h->prof_ev[e0 + 1]));
-          // launches alternate stream pass / link pass; the sharded
-          // epilogue (last launch) counts as link pass.
-          if ((l & 1) == 0 && l < 2 * h->nb())
-            h->prof_ms_k1 += t;
-          else
-            h->prof_ms_k2 += t;
-        }
-        h->prof_iters += 1;
-      }
-      k_seen = c.run_k;
-      done = c.done != 0;
-      inflight = 0;
-    } else if (inflight == 2) {
+    if (inflight == 2) {
       const int prev = slot ^ 1;
       CK(cudaEventSynchronize(h->ev_batch[prev]));
+      if (h->profiling) account(prev, h->ctrl_host[prev]);
       done = h->ctrl_host[prev].done != 0;
       --inflight;
     }
     slot ^= 1;
+  }
+  if (h->profiling) {  // the last batch queued (ran nothing if `done` was already set)
+    CK(cudaEventSynchronize(h->ev_batch[slot ^ 1]));
+    account(slot ^ 1, h->ctrl_host[slot ^ 1]);
   }
   CK(cudaEventRecord(h->ev_run[1], h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -1074,19 +1096,19 @@ int numpmp_gpu_export_layout(numpmp_gpu* h, int64_t* link_offsets, int64_t* link
     // The global link-major CSR built on the device exactly as the column
     // blocks are, plus the terminal ids the sort carried along.
     int64_t tmpb = 0;
-    int* rp = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb);
-    int* ci = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb);
+    int* rp = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
+    int* ci = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &tmpb, h->stream);
     std::vector<int> row_ptr(static_cast<size_t>(m) + 1), terms(static_cast<size_t>(nnz));
     try {
       build_csr(h, 0, h->n, rp, ci, terms.data());
       CK(cudaMemcpy(row_ptr.data(), rp, 4 * (m + 1), cudaMemcpyDeviceToHost));
     } catch (...) {
-      cudaFree(rp);
-      cudaFree(ci);
+      cudaFreeAsync(rp, h->stream);
+      cudaFreeAsync(ci, h->stream);
       throw;
     }
-    cudaFree(rp);
-    cudaFree(ci);
+    cudaFreeAsync(rp, h->stream);
+    cudaFreeAsync(ci, h->stream);
     // model.hpp:182-199: |l| = degree + 1, slack terminal nnz + l last.
     link_offsets[0] = 0;
     for (int64_t l = 0; l < m; ++l) {
@@ -1161,30 +1183,39 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   PhaseTimer pt;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
+                             h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
+                             h->Lacc,    h->Lbuf,    h->k1_part,   h->k2_part,    h->scratch_m,
+                             h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
   for (int i = 0; i < 2; ++i) {
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
-    if (h->prof_graph[i]) cudaGraphExecDestroy(h->prof_graph[i]);
+    for (int set = 0; set < 2; ++set)
+      if (h->prof_graph[i][set]) cudaGraphExecDestroy(h->prof_graph[i][set]);
     if (h->ev_batch[i]) cudaEventDestroy(h->ev_batch[i]);
     if (h->ev_run[i]) cudaEventDestroy(h->ev_run[i]);
-    cudaFree(h->A[i]);
-    cudaFree(h->B[i]);
-    cudaFree(h->zs[i]);
-    cudaFree(h->pr[i]);
-    cudaFree(h->Q[i]);
+    for (void* p : {static_cast<void*>(h->A[i]), static_cast<void*>(h->B[i]),
+                    static_cast<void*>(h->zs[i]), static_cast<void*>(h->pr[i]),
+                    static_cast<void*>(h->Q[i])})
+      bufs.push_back(p);
   }
   for (auto& e : h->prof_ev) cudaEventDestroy(e);
   for (ColBlock& cb : h->blocks) {
-    cudaFree(cb.row_ptr);
-    cudaFree(cb.col_idx);
+    bufs.push_back(cb.row_ptr);
+    bufs.push_back(cb.col_idx);
   }
-  void* bufs[] = {h->col_ptr, h->row_idx,   h->w,         h->kind,      h->deg,      h->cap,
-                  h->x,       h->v,         h->ps0,       h->pbar0,     h->Lacc,     h->Lbuf,
-                  h->k1_part, h->k2_part,   h->scratch_m, h->scratch_m2, h->scratch_n, h->scalars,
-                  h->ctrl,    h->trace_dev};
-  for (void* p : bufs) cudaFree(p);
+  for (void* p : bufs)  // back to the (retained) stream-ordered pool
+    if (p) {
+      if (h->stream)
+        cudaFreeAsync(p, h->stream);
+      else
+        cudaFree(p);
+    }
   if (h->ctrl_host) cudaFreeHost(h->ctrl_host);
   if (h->comm) nccl().CommDestroy(h->comm);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->stream) {
+    cudaStreamSynchronize(h->stream);
+    cudaStreamDestroy(h->stream);
+  }
   delete h;
   pt.mark("destroy");
 }

@@ -480,6 +480,24 @@ def test_config_b_iterations_match_oracle(restatement, oracle_mod):
 
 
 @pytest.mark.slow
+def test_config_c_first_iterations_match_oracle(restatement, oracle_mod):
+    # BASELINE.json configs[2] at full size (100M nonzeros), K = 5 iterations
+    p = _gen(1000000, 10000000, 10.0, 2, True, 7)
+    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0, max_iters=5, trace_every=1)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations == 5
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
+    assert len(sol.trace) == ref.trace.shape[0] == 5
+    for row, want in zip(sol.trace, ref.trace):
+        assert abs(row.r_norm - want[1]) <= RTOL * want[1] and abs(row.s_norm - want[2]) <= RTOL * want[2]
+        assert abs(row.objective - want[4]) <= RTOL * abs(want[4])
+
+
+@pytest.mark.slow
 def test_config_c_full_solve_properties():
     # BASELINE.json configs[2] at full size: converged run is feasible within
     # tolerance and satisfies complementary slackness (test_solver.cpp:417-472)
