@@ -313,6 +313,22 @@ def run_ours(args):
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     iter_ms = (ms1.value + ms2.value) / n_it
     iter_gbs = (k1b + k2b) / (iter_ms * 1e-3) / 1e9
+    # DRAM traffic of the dominant kernel per iteration, from the committed
+    # ncu --set full capture (profiles/traffic_r1.json; config C, one GPU)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_r1.json")) as f:
+            tr = json.load(f)
+        if tr.get("config") == name and world == 1:
+            key = "k_link_pass" if avg2 >= avg1 else "k_stream_pass"
+            traffic = tr["per_iteration"][key]["dram_bytes"]
+    except Exception:
+        traffic = None
+    # The structural bound: one random 8-byte gather per nonzero and pass,
+    # at the measured B200 gather ceiling (scripts/gather_bench.cu,
+    # profiles/r1_gather_microbench.txt: 271 G/s from an L2-resident vector).
+    gather_peak = 271.0e9
+    gather_rate = lp.nnz / (dom_ms * 1e-3)
 
     # e2e: the public C-ABI from pinned host buffers, per step:
     # create (H2D problem + device CSR build) -> solve -> D2H solution -> destroy
@@ -381,8 +397,12 @@ def run_ours(args):
             "wall_s_timed": wall,
             "gen_s": t_gen,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
-                         "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms},
+                         "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": traffic,
+                         "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                         "launch": "one pass over all column blocks per iteration",
+                         "gather_bound": {"achieved_gathers_per_s": gather_rate, "peak_gathers_per_s": gather_peak,
+                                          "frac": gather_rate / gather_peak,
+                                          "source": "scripts/gather_bench.cu (profiles/r1_gather_microbench.txt)"}},
             "iteration_roofline": {"alg_bytes": k1b + k2b, "ms": iter_ms, "achieved_gbs": iter_gbs,
                                    "frac": iter_gbs / hbm, "stream_pass_ms": avg1, "link_pass_ms": avg2},
             "gpu_launches": int(launches.value) + args.steps,

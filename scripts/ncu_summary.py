@@ -24,9 +24,10 @@ want = [
     ("regs", "launch__registers_per_thread"),
     ("smem_bank_conf", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
 ]
-print("kernel," + ",".join(k for k, _ in want))
+w = csv.writer(sys.stdout)
+w.writerow(["kernel"] + [k for k, _ in want])
 for d in data:
-    name = d[idx["Kernel Name"]][:40]
+    name = d[idx["Kernel Name"]].split("(")[0].replace("void ", "")
     vals = []
     for k, m in want:
         if m not in idx:
@@ -41,4 +42,4 @@ for d in data:
             vals.append(f"{f:.1f}")
         except ValueError:
             vals.append(v)
-    print(name + "," + ",".join(vals))
+    w.writerow([name] + vals)
