@@ -41,7 +41,7 @@ constexpr int STAGES = 2;
 __global__ void __launch_bounds__(WARPS * 32) k_tma(const __grid_constant__ CUtensorMap tmap,
                                                    const int* __restrict__ idx, long long n,
                                                    double* sink) {
-  __shared__ __align__(128) double buf[WARPS][STAGES][BATCH * 2];
+  __shared__ __align__(128) double buf[WARPS][STAGES][BATCH * 4];  // 128-B aligned gather4 slots
   __shared__ __align__(8) uint64_t bar[WARPS][STAGES];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0)
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_tma(const __grid_constant__ CUte
                    "r"(BATCH * 16) : "memory");
     __syncwarp();
     // rows = id >> 1 ; every lane issues its own gather4 (4 rows)
-    const uint32_t dst = smem_u32(&buf[w][s][8 * lane]);
+    const uint32_t dst = smem_u32(&buf[w][s][16 * lane]);
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(&tmap), "r"(0), "r"(ids.x >> 1),
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_tma(const __grid_constant__ CUte
           : "=r"(done) : "r"(smem_u32(&bar[w][s])), "r"(phase[s]) : "memory");
     }
     phase[s] ^= 1;
-    const double* row = &buf[w][s][8 * lane];
+    const double* row = &buf[w][s][16 * lane];
     acc += row[0 + (cur_ids.x & 1)] + row[2 + (cur_ids.y & 1)] + row[4 + (cur_ids.z & 1)] +
            row[6 + (cur_ids.w & 1)];
     __syncwarp();
