@@ -31,7 +31,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-constexpr int WARPS = 8;
+constexpr int WARPS = 4;
 constexpr int BATCH = 128;   // indices per warp per round
 constexpr int STAGES = 2;
 
