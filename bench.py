@@ -42,6 +42,8 @@ CONFIGS = {
               desc="C: 10M streams / 1M links, mixed log+linear (Bernoulli 0.5), w~U(0.5,1.5)"),
     "D": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, degrade=(0.5, 0.5, 99),
               desc="D: C with 50% of capacities x0.5 (degrade seed 99)"),
+    "E": dict(transit=(100, 192, 5.0, 952, 9900, 9, 192, 50.0, 4), rho0=1000.0,
+              desc="E: time-expanded transit, S=100 T=192 |E|=952, 9900 OD x 9 routes x 192 departures, seats 50"),
 }
 
 
@@ -58,6 +60,9 @@ def make_problem(name):
     import paper_2509_10722_b200 as pmp
 
     c = CONFIGS[name]
+    if "transit" in c:
+        p, _ = pmp.gen_transit(pmp.TransitSpec(*c["transit"]))
+        return p
     w = pmp.WeightDist.uniform(0.5, 1.5) if c["uniform"] else pmp.WeightDist.constant(1.0)
     p = pmp.gen_uncongested(pmp.GenSpec(m=c["m"], n=c["n"], avg_links_per_stream=c["avg"],
                                         kind=pmp.GenKind(c["kind"]), weights=w, seed=c["seed"]))

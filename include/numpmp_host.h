@@ -47,6 +47,26 @@ void numpmp_instance_export(const numpmp_instance* inst, double* capacities, dou
                             uint8_t* kinds, int64_t* stream_offsets, int32_t* route_links);
 void numpmp_instance_free(numpmp_instance* inst);
 
+/* TransitSpec (transit.hpp:22-32): time-expanded transit network, one
+ * stream per (OD pair, route, departure); link id = edge * time_bins + t. */
+typedef struct {
+  int32_t stations;
+  int32_t time_bins;
+  double bin_minutes;
+  int64_t spatial_edges;
+  int64_t od_pairs;
+  int32_t routes_per_od;
+  int32_t departures_per_route;
+  double seats;
+  uint64_t seed;
+} numpmp_transit_spec;
+
+/* gen_transit (transit.hpp:152-287): random strongly connected spatial
+ * graph, Yen k-shortest loop-free routes per OD pair, evenly spaced
+ * departures; streams arriving past the horizon are dropped (count in
+ * *dropped).  Returns 0 or 5 (GenError). */
+int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, int64_t* dropped);
+
 /* In-place capacity degradation with the reference's draw order. */
 int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor, uint64_t seed);
 

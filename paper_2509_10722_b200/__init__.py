@@ -15,10 +15,12 @@ from .model import (
     Stream,
     StreamKind,
     TerminalLayout,
+    TransitSpec,
     WeightDist,
     build_problem,
     degrade,
     gen_congested,
+    gen_transit,
     gen_uncongested,
     problem_from_arrays,
     validate,
@@ -40,8 +42,8 @@ from .solver import (
 
 __all__ = [
     "DeviceError", "DomainError", "GenError", "SolverError", "ValidationError",
-    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "WeightDist",
-    "build_problem", "degrade", "gen_congested", "gen_uncongested", "problem_from_arrays", "validate",
+    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitSpec", "WeightDist",
+    "build_problem", "degrade", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "validate",
     "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
     "check_termination", "objective", "recover_duals", "to_string", "update_rho",
 ]

@@ -79,6 +79,20 @@ class GenSpecC(C.Structure):
     ]
 
 
+class TransitSpecC(C.Structure):
+    _fields_ = [
+        ("stations", C.c_int32),
+        ("time_bins", C.c_int32),
+        ("bin_minutes", C.c_double),
+        ("spatial_edges", C.c_int64),
+        ("od_pairs", C.c_int64),
+        ("routes_per_od", C.c_int32),
+        ("departures_per_route", C.c_int32),
+        ("seats", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
 P = C.c_void_p
 I64 = C.c_int64
 D = C.c_double
@@ -114,6 +128,7 @@ SIGNATURES = {
     "numpmp_instance_sizes": (None, [P, PI64, PI64, PI64]),
     "numpmp_instance_export": (None, [P, P, P, P, P, P]),
     "numpmp_instance_free": (None, [P]),
+    "numpmp_gen_transit": (C.c_int, [C.POINTER(TransitSpecC), C.POINTER(P), PI64]),
     "numpmp_degrade": (C.c_int, [I64, P, D, D, C.c_uint64]),
     "numpmp_validate": (I64, [I64, I64, P, P, P, P, P, C.c_char_p, I64]),
     "numpmp_build_layout": (C.c_int, [I64, I64, P, P, P, P, P, P]),

@@ -233,6 +233,204 @@ int numpmp_gen_congested(const numpmp_gen_spec* spec, double hot_link_fraction,
   }
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------- transit
+// transit.hpp:62-287 restated: the same RNG draws, the same BFS
+// tie-breaking (neighbours in sorted adjacency order) and the same Yen
+// candidate order (by length, then node sequence), hence the same streams.
+namespace {
+
+using Adj = std::vector<std::vector<std::pair<std::int32_t, std::int32_t>>>;  // (to, edge)
+
+// Unit-weight BFS path src -> dst avoiding banned nodes / (from, to) edges.
+std::vector<std::int32_t> bfs_path(const Adj& adj, std::int32_t src, std::int32_t dst,
+                                   const std::vector<char>& node_banned,
+                                   const std::vector<std::pair<std::int32_t, std::int32_t>>& edge_banned) {
+  const std::size_t n = adj.size();
+  std::vector<std::int32_t> parent(n, -2);
+  std::vector<std::int32_t> queue;
+  queue.reserve(n);
+  parent[static_cast<std::size_t>(src)] = -1;
+  queue.push_back(src);
+  for (std::size_t head = 0; head < queue.size(); ++head) {
+    const std::int32_t v = queue[head];
+    if (v == dst) break;
+    for (const auto& te : adj[static_cast<std::size_t>(v)]) {
+      const std::int32_t to = te.first;
+      if (node_banned[static_cast<std::size_t>(to)]) continue;
+      if (std::find(edge_banned.begin(), edge_banned.end(), std::make_pair(v, to)) != edge_banned.end())
+        continue;
+      if (parent[static_cast<std::size_t>(to)] != -2) continue;
+      parent[static_cast<std::size_t>(to)] = v;
+      queue.push_back(to);
+    }
+  }
+  if (parent[static_cast<std::size_t>(dst)] == -2) return {};
+  std::vector<std::int32_t> path;
+  for (std::int32_t v = dst; v != -1; v = parent[static_cast<std::size_t>(v)]) path.push_back(v);
+  std::reverse(path.begin(), path.end());
+  return path;
+}
+
+bool shorter_or_lex_less(const std::vector<std::int32_t>& a, const std::vector<std::int32_t>& b) {
+  if (a.size() != b.size()) return a.size() < b.size();
+  return a < b;
+}
+
+// Yen's k loop-free shortest paths; candidates kept as a sorted unique list.
+std::vector<std::vector<std::int32_t>> k_shortest(const Adj& adj, std::int32_t src, std::int32_t dst,
+                                                  std::int32_t k) {
+  std::vector<std::vector<std::int32_t>> found;
+  const std::vector<char> no_ban(adj.size(), 0);
+  std::vector<std::int32_t> first = bfs_path(adj, src, dst, no_ban, {});
+  if (first.empty()) return found;
+  found.push_back(std::move(first));
+  std::vector<std::vector<std::int32_t>> cand;  // sorted by (length, sequence), unique
+  while (static_cast<std::int32_t>(found.size()) < k) {
+    const std::vector<std::int32_t> last = found.back();
+    for (std::size_t spur = 0; spur + 1 < last.size(); ++spur) {
+      std::vector<std::int32_t> root(last.begin(), last.begin() + static_cast<std::ptrdiff_t>(spur) + 1);
+      std::vector<std::pair<std::int32_t, std::int32_t>> banned_edges;
+      for (const auto& p : found)
+        if (p.size() > spur + 1 && std::equal(root.begin(), root.end(), p.begin()))
+          banned_edges.emplace_back(p[spur], p[spur + 1]);
+      std::vector<char> banned_nodes(adj.size(), 0);
+      for (std::size_t i = 0; i < spur; ++i) banned_nodes[static_cast<std::size_t>(root[i])] = 1;
+      std::vector<std::int32_t> tail = bfs_path(adj, root.back(), dst, banned_nodes, banned_edges);
+      if (tail.empty()) continue;
+      root.pop_back();
+      root.insert(root.end(), tail.begin(), tail.end());
+      if (std::find(found.begin(), found.end(), root) != found.end()) continue;
+      auto pos = std::lower_bound(cand.begin(), cand.end(), root, shorter_or_lex_less);
+      if (pos == cand.end() || shorter_or_lex_less(root, *pos)) cand.insert(pos, std::move(root));
+    }
+    if (cand.empty()) break;
+    found.push_back(cand.front());
+    cand.erase(cand.begin());
+  }
+  return found;
+}
+
+}  // namespace
+
+extern "C" {
+
+int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, int64_t* dropped) {
+  const std::int32_t S = spec->stations, T = spec->time_bins;
+  const std::int64_t E = spec->spatial_edges;
+  auto gen_error = [](const char* msg) {
+    g_host_err = msg;
+    return 5;
+  };
+  // transit.hpp:155-171
+  if (S < 2) return gen_error("transit spec: stations must be >= 2");
+  if (T < 1) return gen_error("transit spec: time_bins must be >= 1");
+  if (!(spec->bin_minutes > 0.0)) return gen_error("transit spec: bin_minutes must be > 0");
+  if (E < S) return gen_error("transit spec: need at least S edges for strong connectivity");
+  if (E > std::int64_t(S) * (S - 1)) return gen_error("transit spec: more edges than ordered station pairs");
+  if (spec->od_pairs < 1 || spec->od_pairs > std::int64_t(S) * (S - 1))
+    return gen_error("transit spec: od_pairs out of range");
+  if (spec->routes_per_od < 1) return gen_error("transit spec: routes_per_od must be >= 1");
+  if (spec->departures_per_route < 1) return gen_error("transit spec: departures_per_route must be >= 1");
+  if (!(spec->seats > 0.0)) return gen_error("transit spec: seats must be > 0");
+  try {
+    Rng rng(spec->seed);
+    // random permutation cycle, then distinct random extra edges (transit.hpp:179-203)
+    std::vector<std::int32_t> perm(static_cast<std::size_t>(S));
+    for (std::int32_t v = 0; v < S; ++v) perm[static_cast<std::size_t>(v)] = v;
+    for (std::int32_t i = S - 1; i > 0; --i) {
+      const std::int64_t j = rng.uniform_int(i + 1);
+      std::swap(perm[static_cast<std::size_t>(i)], perm[static_cast<std::size_t>(j)]);
+    }
+    std::vector<std::pair<std::int32_t, std::int32_t>> edges;
+    std::vector<char> has_edge(static_cast<std::size_t>(S) * S, 0);
+    auto add_edge = [&](std::int32_t f, std::int32_t t) {
+      edges.emplace_back(f, t);
+      has_edge[static_cast<std::size_t>(f) * S + t] = 1;
+    };
+    for (std::int32_t i = 0; i < S; ++i)
+      add_edge(perm[static_cast<std::size_t>(i)], perm[static_cast<std::size_t>((i + 1) % S)]);
+    std::int64_t guard = 0;
+    while (std::int64_t(edges.size()) < E) {
+      const std::int32_t f = static_cast<std::int32_t>(rng.uniform_int(S));
+      const std::int32_t t = static_cast<std::int32_t>(rng.uniform_int(S));
+      if (f == t || has_edge[static_cast<std::size_t>(f) * S + t]) {
+        if (++guard > 100LL * S * S) return gen_error("transit spec: could not place the requested edges");
+        continue;
+      }
+      add_edge(f, t);
+    }
+    Adj adj(static_cast<std::size_t>(S));
+    for (std::int32_t e = 0; e < std::int32_t(edges.size()); ++e)
+      adj[static_cast<std::size_t>(edges[static_cast<std::size_t>(e)].first)].emplace_back(
+          edges[static_cast<std::size_t>(e)].second, e);
+    for (auto& nb : adj) std::sort(nb.begin(), nb.end());
+    // OD pairs and their k shortest routes as edge sequences (transit.hpp:205-246)
+    std::vector<char> od_used(static_cast<std::size_t>(S) * S, 0);
+    std::int64_t od_count = 0;
+    std::vector<std::vector<std::vector<std::int32_t>>> od_routes;
+    guard = 0;
+    while (od_count < spec->od_pairs) {
+      const std::int32_t o = static_cast<std::int32_t>(rng.uniform_int(S));
+      const std::int32_t d = static_cast<std::int32_t>(rng.uniform_int(S));
+      if (o == d || od_used[static_cast<std::size_t>(o) * S + d]) {
+        if (++guard > 100LL * S * S) return gen_error("transit spec: could not place the requested OD pairs");
+        continue;
+      }
+      od_used[static_cast<std::size_t>(o) * S + d] = 1;
+      ++od_count;
+      const auto paths = k_shortest(adj, o, d, spec->routes_per_od);
+      if (paths.empty()) continue;  // disconnected OD (a warning in the reference)
+      std::vector<std::vector<std::int32_t>> routes;
+      for (const auto& path : paths) {
+        std::vector<std::int32_t> es;
+        for (std::size_t i = 0; i + 1 < path.size(); ++i) {
+          const auto& nb = adj[static_cast<std::size_t>(path[i])];
+          auto pos = std::lower_bound(nb.begin(), nb.end(), std::make_pair(path[i + 1], std::int32_t(-1)));
+          es.push_back(pos->second);
+        }
+        routes.push_back(std::move(es));
+      }
+      od_routes.push_back(std::move(routes));
+    }
+    if (od_routes.empty()) return gen_error("transit spec: no usable OD pair");
+    // one stream per (OD, route, departure) (transit.hpp:250-279)
+    auto* inst = new numpmp_instance();
+    inst->offsets.push_back(0);
+    std::int64_t drop = 0;
+    for (const auto& routes : od_routes)
+      for (const auto& route : routes)
+        for (std::int32_t dep = 0; dep < spec->departures_per_route; ++dep) {
+          const std::int32_t t0 =
+              static_cast<std::int32_t>((std::int64_t(dep) * T) / spec->departures_per_route);
+          if (t0 + std::int32_t(route.size()) - 1 > T - 1) {
+            ++drop;
+            continue;
+          }
+          for (std::size_t i = 0; i < route.size(); ++i)
+            inst->routes.push_back(static_cast<std::int32_t>(std::int64_t(route[i]) * T + t0 +
+                                                             static_cast<std::int32_t>(i)));
+          inst->offsets.push_back(static_cast<std::int64_t>(inst->routes.size()));
+          inst->kinds.push_back(0);
+          inst->weights.push_back(1.0);
+        }
+    if (inst->kinds.empty()) {
+      delete inst;
+      return gen_error("transit spec: every stream fell outside the horizon");
+    }
+    inst->n = static_cast<std::int64_t>(inst->kinds.size());
+    inst->m = std::int64_t(edges.size()) * T;
+    inst->capacities.assign(static_cast<std::size_t>(inst->m), spec->seats);
+    if (dropped) *dropped = drop;
+    *out = inst;
+    return 0;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return 9;
+  }
+}
+
 void numpmp_instance_sizes(const numpmp_instance* inst, int64_t* m, int64_t* n, int64_t* nnz) {
   *m = inst->m;
   *n = inst->n;

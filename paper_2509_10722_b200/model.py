@@ -222,6 +222,32 @@ def gen_congested(spec: GenSpec, hot_link_fraction=0.001, hot_stream_fraction=0.
     return _from_instance(inst)
 
 
+@dataclass
+class TransitSpec:  # transit.hpp:22-32
+    stations: int = 0
+    time_bins: int = 0
+    bin_minutes: float = 5.0
+    spatial_edges: int = 0
+    od_pairs: int = 0
+    routes_per_od: int = 1
+    departures_per_route: int = 1
+    seats: float = 50.0
+    seed: int = 0
+
+
+def gen_transit(spec: TransitSpec):
+    """transit.hpp:152-287 (bit-identical streams); returns (Problem, dropped)."""
+    L = _lib.lib()
+    inst = C.c_void_p()
+    dropped = C.c_int64()
+    cs = _lib.TransitSpecC(spec.stations, spec.time_bins, spec.bin_minutes, spec.spatial_edges, spec.od_pairs,
+                           spec.routes_per_od, spec.departures_per_route, spec.seats, spec.seed)
+    rc = L.numpmp_gen_transit(C.byref(cs), C.byref(inst), C.byref(dropped))
+    if rc:
+        raise GenError(L.numpmp_host_last_error().decode())
+    return _from_instance(inst), dropped.value
+
+
 def degrade(problem: Problem, p_degrade=0.25, factor=0.5, seed=0) -> Problem:
     """gen.hpp:132-143: structure unchanged, capacities cut."""
     caps = problem.capacities.copy()

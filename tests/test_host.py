@@ -52,6 +52,32 @@ def test_congested_generator_bit_exact(reference):
     np.testing.assert_array_equal(p.capacities, ra.capacities)
 
 
+@pytest.mark.parametrize("args", [
+    (12, 24, 5.0, 30, 40, 3, 24, 50.0, 4),
+    (100, 192, 5.0, 952, 110, 3, 60, 50.0, 4),       # the paper's transit case
+    (30, 48, 5.0, 80, 300, 5, 48, 20.0, 9),
+])
+def test_transit_generator_bit_exact(args, reference):
+    p, dropped = pmp.gen_transit(pmp.TransitSpec(*args))
+    rp = reference.gen_transit(*args)
+    ra = rp.arrays()
+    assert dropped == rp.dropped
+    for mine, theirs in [(p.stream_offsets, ra.stream_offsets), (p.route_links, ra.route_links),
+                         (p.capacities, ra.capacities), (p.weights, ra.weights), (p.kinds, ra.kinds)]:
+        np.testing.assert_array_equal(mine, theirs)
+
+
+@pytest.mark.slow
+def test_transit_config_e_bit_exact(reference):
+    # BASELINE.json configs[4]: m 182,784, n 16,923,949, nnz 51,702,844
+    args = (100, 192, 5.0, 952, 9900, 9, 192, 50.0, 4)
+    p, dropped = pmp.gen_transit(pmp.TransitSpec(*args))
+    assert (p.m, p.n, p.nnz, dropped) == (182784, 16923949, 51702844, 183251)
+    ra = reference.gen_transit(*args).arrays()
+    np.testing.assert_array_equal(p.route_links, ra.route_links)
+    np.testing.assert_array_equal(p.stream_offsets, ra.stream_offsets)
+
+
 def test_degrade_bit_exact(reference):
     case = (500, 2000, 6.0, 2, ("uniform", 0.5, 1.5), 17)
     rd = reference.gen(*case).degrade(0.5, 0.5, 99).arrays()
