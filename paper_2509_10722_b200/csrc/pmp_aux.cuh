@@ -95,27 +95,36 @@ __global__ void k_degree(const int* __restrict__ row_ptr, long long m, int* __re
     deg[l] = row_ptr[l + 1] - row_ptr[l];
 }
 
-// Per-row sums over one column block, accumulated across blocks in block
-// order: out = (first ? 0 : out) + sum_{j in row l, block b} src_j -- the
-// same arithmetic and order as the link pass.
-__global__ void __launch_bounds__(kThreads) k_row_sums(const int* __restrict__ row_ptr,
-                                                       const int* __restrict__ col_idx,
-                                                       const double* __restrict__ src, long long m,
-                                                       double* __restrict__ out, int first) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol = policy_evict_first();
-  const long long ngroups = (m + 31) / 32;
-  for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
-       g += (long long)gridDim.x * kWarps) {
-    const long long r = g * 32 + lane;
-    const bool valid = r < m;
-    const int rb = row_ptr[valid ? r : m];
-    const int re = valid ? row_ptr[r + 1] : rb;
-    const int sb = __shfl_sync(kFull, rb, 0), se = __shfl_sync(kFull, re, 31);
-    const double s = warp_segments_sum(col_idx, sb, se, rb, re, sidx[wib], lane, GatherX{src}, pol);
-    if (valid) out[r] = first ? s : out[r] + s;
+// Column-block segmentation of the link-major CSR ("virtual rows"): link l
+// with d entries in the block gets ceil(d / kSeg) segments of near-equal
+// size.  nseg[l] -> (exclusive scan) row_vstart; then each link writes its
+// segments' CSR starts and its id.
+__global__ void k_seg_count(const int* __restrict__ row_ptr, long long m, int* __restrict__ nseg) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const int d = row_ptr[l + 1] - row_ptr[l];
+    nseg[l] = (d + kSeg - 1) / kSeg;
   }
+}
+__global__ void k_seg_fill(const int* __restrict__ row_ptr, const int* __restrict__ row_vstart,
+                           long long m, int* __restrict__ vptr, int* __restrict__ vrow) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const int b = row_ptr[l], d = row_ptr[l + 1] - b;
+    const int v0 = row_vstart[l], ns = row_vstart[l + 1] - v0;
+    for (int s = 0; s < ns; ++s) {
+      vptr[v0 + s] = b + static_cast<int>((static_cast<long long>(s) * d) / ns);
+      vrow[v0 + s] = static_cast<int>(l);
+    }
+    if (l == m - 1) vptr[v0 + ns] = b + d;
+  }
+}
+
+// L = combined per-link sums of the preceding k_link_gather launches.
+__global__ void k_link_combine(IterArgs a, double* __restrict__ out) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < a.m;
+       l += (long long)gridDim.x * blockDim.x)
+    out[l] = combine_link(a, l);
 }
 
 // warm_start_from (solver.hpp:218-259) in link space, given L = R x0:

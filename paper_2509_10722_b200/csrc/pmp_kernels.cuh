@@ -61,11 +61,15 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
 constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
+constexpr int kSeg = kStageInts / 32;          // max entries per link segment (one staged round per warp)
+constexpr int kMaxBlocks = 16;                 // max column blocks
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { ST_RUNNING = -1, ST_CONVERGED = 0, ST_MAXITERS = 1, ST_TIMELIMIT = 2,
              ST_NONFINITE = 3 };
-enum : int { MODE_RUN = 0, MODE_STEP = 1 };
+// MODE_AUX: a link-pass gather outside the iteration (warm start, state
+// materialisation, post-processing) -- ignores the `done` flag.
+enum : int { MODE_RUN = 0, MODE_STEP = 1, MODE_AUX = 2 };
 
 // Device-resident control block: the run loop of solver.hpp:450-476 lives
 // here, written only by the last block of the link pass.
@@ -114,21 +118,28 @@ struct IterArgs {
   double* v;
   double* k1_part;  // [nb][grid1][2]: tau dA^2, objective
   double* k2_part;  // [grid2][4]: r^2, dB.dQ, d dB^2, dzs^2
-  int grid1, grid2, nblocks;
-  double* Lacc;     // m: running sum of the column blocks' partial loads
+  int grid1, grid2, grid3, nblocks;
+  // per column block: first segment of every link, segment partial sums
+  const int* row_vstart[kMaxBlocks];  // m+1
+  const double* vpart[kMaxBlocks];    // per-segment partials (row tails only)
   double* Lbuf;     // sharded: m partial loads + 2 scalars
   Ctrl* ctrl;
   numpmp_trace_row* trace;
   long long trace_cap;
 };
 
-// One column block: streams [s0, s1) and the CSR of their columns.
+// One column block: streams [s0, s1), the CSR of their columns, and its
+// segmentation into "virtual rows" of at most kSeg consecutive entries of
+// one link (rows split evenly), so every lane's gather chain is bounded
+// whatever the link degree skew.
 struct BlockArgs {
   long long s0, s1;
-  const int* row_ptr;  // m+1 into col_idx
   const int* col_idx;  // global stream ids, ascending per row
+  const int* vptr;     // nv+1: first CSR entry of each segment
+  const int* vrow;     // nv: link of each segment
+  double* vpart;       // nv: in-warp partial of the row at its tail segment
+  long long nv;
   int index;           // block number b
-  int first;           // b == 0
 };
 
 // ---------------------------------------------------------------- helpers
@@ -373,6 +384,42 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
 }
 
 // --------------------------------------------------------------- K2: links
+// Link-pass gather over one column block: one lane per segment (<= kSeg
+// entries of one link), a warp per 32 consecutive segments (their index
+// span is one staged round).  The segments of a link are adjacent lanes; a
+// fixed-order segmented inclusive scan over the lanes leaves the warp's
+// partial for each link at its last segment in the warp ("tail"), which is
+// stored at vpart[tail].  The epilogue kernel folds the tails of a link
+// (one per warp the link spans, per column block) in a fixed order.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_gather(IterArgs a, BlockArgs bk,
+                                                                     const double* __restrict__ src) {
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
+  if (a.mode != MODE_AUX && kernel_should_exit(a.ctrl)) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol_first = policy_evict_first();
+  const long long nunits = (bk.nv + 31) / 32;
+  for (long long u = (long long)blockIdx.x * kWarps + wib; u < nunits;
+       u += (long long)gridDim.x * kWarps) {
+    const long long v = u * 32 + lane;
+    const bool valid = v < bk.nv;
+    const int vb = __ldg(bk.vptr + (valid ? v : bk.nv));
+    const int ve = valid ? __ldg(bk.vptr + v + 1) : vb;
+    const int row = valid ? __ldg(bk.vrow + v) : -1;
+    const int span_beg = __shfl_sync(kFull, vb, 0);
+    const int span_end = __shfl_sync(kFull, ve, 31);
+    double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
+                                 GatherX{src}, pol_first);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
+      const double t = __shfl_up_sync(kFull, s, d);
+      const int tr = __shfl_up_sync(kFull, row, d);
+      if (lane >= d && tr == row) s += t;
+    }
+    const int next_row = __shfl_down_sync(kFull, row, 1);
+    if (valid && (lane == 31 || next_row != row)) __stcg(bk.vpart + v, s);
+  }
+}
+
 // Per-link epilogue: slack projection (solver.hpp:368-376), link average
 // (110-126), z update split into B / zs / Q (388-399), price (401-405).
 __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, double L, int d,
@@ -404,6 +451,20 @@ __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, do
   a.Q_out[r] = Qn;
   a.pr_out[r] = prn;
   st_hint_f64(a.v + r, Bn + prn / rho, pol_last);
+}
+
+// L_l = sum over column blocks (in order) of the block's tails for link l
+// (one per 32-segment warp unit the link spans, in order).
+__device__ __forceinline__ double combine_link(const IterArgs& a, long long l) {
+  double L = 0.0;
+  for (int b = 0; b < a.nblocks; ++b) {
+    const int rs = __ldg(a.row_vstart[b] + l), re = __ldg(a.row_vstart[b] + l + 1);
+    if (re <= rs) continue;
+    double Lb = 0.0;
+    for (int k = rs >> 5; k <= (re - 1) >> 5; ++k) Lb += __ldcg(a.vpart[b] + min(re - 1, 32 * k + 31));
+    L += Lb;
+  }
+  return L;
 }
 
 // Finalize one iteration on the device: r, s, then the exact control order
@@ -461,60 +522,32 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
   }
 }
 
-// Link-pass phases.
-//   LP_ACC      : gather over column block b, L partial -> Lacc (b < NB-1).
-//   LP_FUSED    : gather over the last block, L = Lacc + partial, epilogue,
-//                 residual partials, last-block finalize (single GPU).
-//   LP_GATHER   : sharded, last block: local loads -> Lbuf (+ K1 scalars),
-//                 then the NCCL all-reduce.
-//   LP_EPILOGUE : sharded, replicated epilogue on the all-reduced loads.
-enum : int { LP_ACC = 0, LP_FUSED = 1, LP_GATHER = 2, LP_EPILOGUE = 3 };
+// Link epilogue phases (one thread per link, grid-stride).
+//   EP_FUSED    : combine the blocks' tails, epilogue, residual partials,
+//                 last-block finalize (single GPU).
+//   EP_COMBINE  : sharded: local loads -> Lbuf, the last block folds the
+//                 stream-pass scalars into Lbuf[m], Lbuf[m+1]; NCCL next.
+//   EP_EPILOGUE : sharded: replicated epilogue on the all-reduced Lbuf.
+enum : int { EP_FUSED = 0, EP_COMBINE = 1, EP_EPILOGUE = 2 };
 
 template <int kPhase>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts];
+__global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
   __shared__ bool s_last;
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
-  const long long ngroups = (a.m + 31) / 32;
   double part[4] = {0.0, 0.0, 0.0, 0.0};
-  for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
-       g += (long long)gridDim.x * kWarps) {
-    const long long r = g * 32 + lane;
-    const bool valid = r < a.m;
-    double L;
-    if (kPhase == LP_EPILOGUE) {
-      if (!valid) continue;
-      L = __ldcg(a.Lbuf + r);
-    } else {
-      const int rb = __ldg(bk.row_ptr + (valid ? r : a.m));
-      const int re = valid ? __ldg(bk.row_ptr + r + 1) : rb;
-      double prev = 0.0;
-      if (!bk.first && valid) prev = __ldcg(a.Lacc + r);
-      const int span_beg = __shfl_sync(kFull, rb, 0);
-      const int span_end = __shfl_sync(kFull, re, 31);
-      const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
-                                         GatherX{a.x}, pol_first);
-      if (!valid) continue;
-      L = bk.first ? s : prev + s;
-      if (kPhase == LP_ACC) {
-        __stcg(a.Lacc + r, L);
-        continue;
-      }
-      if (kPhase == LP_GATHER) {
-        a.Lbuf[r] = L;
-        continue;
-      }
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.m;
+       r += (long long)gridDim.x * blockDim.x) {
+    if (kPhase == EP_COMBINE) {
+      a.Lbuf[r] = combine_link(a, r);
+      continue;
     }
+    const double L = (kPhase == EP_EPILOGUE) ? __ldcg(a.Lbuf + r) : combine_link(a, r);
     link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
   }
-  if (kPhase == LP_ACC) return;
-  if (kPhase == LP_GATHER) {
-    // The last block folds K1's scalar partials into Lbuf[m], Lbuf[m+1] so
-    // one all-reduce carries loads and scalars.
+  if (kPhase == EP_COMBINE) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket2, 1u) == gridDim.x - 1);
@@ -537,17 +570,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   if (!s_last) return;
   __threadfence();
   double tda2, obj;
-  if (kPhase == LP_EPILOGUE) {
+  if (kPhase == EP_EPILOGUE) {
     tda2 = __ldcg(a.Lbuf + a.m);
     obj = __ldcg(a.Lbuf + a.m + 1);
   } else {
     tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
     obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
   }
-  const double r2 = block_sum_array(a.k2_part, a.grid2, 4, 0);
-  const double cross = block_sum_array(a.k2_part, a.grid2, 4, 1);
-  const double ddb2 = block_sum_array(a.k2_part, a.grid2, 4, 2);
-  const double dzs2 = block_sum_array(a.k2_part, a.grid2, 4, 3);
+  const double r2 = block_sum_array(a.k2_part, a.grid3, 4, 0);
+  const double cross = block_sum_array(a.k2_part, a.grid3, 4, 1);
+  const double ddb2 = block_sum_array(a.k2_part, a.grid3, 4, 2);
+  const double dzs2 = block_sum_array(a.k2_part, a.grid3, 4, 3);
   if (threadIdx.x == 0) {
     finalize_iteration(a, rho, tda2, obj, r2, cross, ddb2, dzs2);
     a.ctrl->ticket = 0;

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "numpmp_gpu.h"
 #include "numpmp_host.h"
@@ -136,9 +137,13 @@ struct PhaseTimer {
 
 // One column block of the device problem (see pmp_kernels.cuh).
 struct ColBlock {
-  int64_t s0 = 0, s1 = 0, nnz = 0;
-  int* row_ptr = nullptr;  // m+1
-  int* col_idx = nullptr;  // nnz + pad, global stream ids
+  int64_t s0 = 0, s1 = 0, nnz = 0, nv = 0;
+  int* row_ptr = nullptr;     // m+1
+  int* col_idx = nullptr;     // nnz + pad, global stream ids
+  int* row_vstart = nullptr;  // m+1: first segment of each link
+  int* vptr = nullptr;        // nv+1
+  int* vrow = nullptr;        // nv
+  double* vpart = nullptr;    // nv
 };
 
 }  // namespace
@@ -174,7 +179,6 @@ struct numpmp_gpu {
   double* v = nullptr;
   double* ps0 = nullptr;    // slack flows of an uploaded state
   double* pbar0 = nullptr;  // link averages of an uploaded state
-  double* Lacc = nullptr;   // m
   double* Lbuf = nullptr;   // m + 2
   double* k1_part = nullptr;
   double* k2_part = nullptr;
@@ -188,7 +192,7 @@ struct numpmp_gpu {
   int64_t trace_cap = 0;
 
   int cur = 0;  // index of the current iterate buffers
-  int grid1 = 0, grid2 = 0;
+  int grid1 = 0, grid2 = 0, grid3 = 0;
   int64_t iters_since_upload = 0;
   bool host_p_valid = false;  // set_state keeps p / p_bar verbatim for get_state
   std::vector<double> host_p, host_pbar;
@@ -209,7 +213,7 @@ struct numpmp_gpu {
 
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
-  int launches_per_iteration() const { return 2 * nb() + (sharded ? 1 : 0); }
+  int launches_per_iteration() const { return 2 * nb() + (sharded ? 2 : 1); }
 };
 
 namespace {
@@ -272,8 +276,12 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.k2_part = h->k2_part;
   a.grid1 = h->grid1;
   a.grid2 = h->grid2;
+  a.grid3 = h->grid3;
   a.nblocks = h->nb();
-  a.Lacc = h->Lacc;
+  for (int b = 0; b < h->nb(); ++b) {
+    a.row_vstart[b] = h->blocks[static_cast<size_t>(b)].row_vstart;
+    a.vpart[b] = h->blocks[static_cast<size_t>(b)].vpart;
+  }
   a.Lbuf = h->Lbuf;
   a.ctrl = h->ctrl;
   a.trace = h->trace_dev;
@@ -286,10 +294,12 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   BlockArgs k{};
   k.s0 = cb.s0;
   k.s1 = cb.s1;
-  k.row_ptr = cb.row_ptr;
   k.col_idx = cb.col_idx;
+  k.vptr = cb.vptr;
+  k.vrow = cb.vrow;
+  k.vpart = cb.vpart;
+  k.nv = cb.nv;
   k.index = b;
-  k.first = b == 0;
   return k;
 }
 
@@ -314,26 +324,26 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
     CK(cudaGetLastError());
     mark();
-    if (b + 1 < nb)
-      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk);
-    else if (!h->sharded)
-      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk);
-    else
-      k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk);
+    k_link_gather<<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x);
     CK(cudaGetLastError());
     mark();
   }
-  if (h->sharded) {
+  if (!h->sharded) {
+    k_link_epilogue<EP_FUSED><<<h->grid3, kThreads, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+    mark();
+  } else {
+    k_link_epilogue<EP_COMBINE><<<h->grid3, kThreads, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+    mark();
     NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum, h->comm,
                  h->stream));
-    k_link_pass<LP_EPILOGUE><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, 0));
+    k_link_epilogue<EP_EPILOGUE><<<h->grid3, kThreads, 0, h->stream>>>(a);
     CK(cudaGetLastError());
     mark();
   }
 }
 
-// ev_set < 0: no events; else the graph records event set ev_set
-// (1 + kBatchIters * launches_per_iteration events) around every launch.
 cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
   cudaGraph_t g = nullptr;
   const int lpi = h->launches_per_iteration();
@@ -374,11 +384,13 @@ Ctrl read_ctrl(numpmp_gpu* h) {
 // Per-link sums of src over this device's columns, block by block in the
 // same order as the link pass (+ NCCL sum when sharded).
 void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
+  IterArgs a = make_args(h, h->cur, MODE_AUX);
   for (int b = 0; b < h->nb(); ++b) {
-    const ColBlock& cb = h->blocks[static_cast<size_t>(b)];
-    k_row_sums<<<h->grid2, kThreads, 0, h->stream>>>(cb.row_ptr, cb.col_idx, src, h->m, out, b == 0);
+    k_link_gather<<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src);
     CK(cudaGetLastError());
   }
+  k_link_combine<<<h->grid3, kThreads, 0, h->stream>>>(a, out);
+  CK(cudaGetLastError());
   if (h->sharded)
     NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm, h->stream));
 }
@@ -464,6 +476,35 @@ int choose_blocks(int64_t n) {
   return static_cast<int>(std::min<int64_t>(nb, std::max<int64_t>(1, n / 32)));
 }
 
+// Virtual-row segmentation of one column block's CSR (pmp_kernels.cuh).
+void segment_block(numpmp_gpu* h, ColBlock& cb) {
+  const int64_t m = h->m;
+  int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &h->dev_bytes, h->stream);
+  cb.row_vstart = dalloc<int>(static_cast<size_t>(m) + 1, &h->dev_bytes, h->stream);
+  CK(cudaMemsetAsync(nseg + m, 0, sizeof(int), h->stream));
+  k_seg_count<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, nseg);
+  CK(cudaGetLastError());
+  size_t temp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, nseg, cb.row_vstart, static_cast<int>(m + 1),
+                                   h->stream));
+  void* temp = nullptr;
+  CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
+  CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nseg, cb.row_vstart, static_cast<int>(m + 1),
+                                   h->stream));
+  int nv = 0;
+  CK(cudaMemcpyAsync(&nv, cb.row_vstart + m, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFreeAsync(temp, h->stream);
+  cudaFreeAsync(nseg, h->stream);
+  cb.nv = nv;
+  cb.vptr = dalloc<int>(static_cast<size_t>(nv) + 1, &h->dev_bytes, h->stream);
+  cb.vrow = dalloc<int>(static_cast<size_t>(nv), &h->dev_bytes, h->stream);
+  cb.vpart = dalloc<double>(static_cast<size_t>(nv), &h->dev_bytes, h->stream);
+  if (nv == 0) CK(cudaMemsetAsync(cb.vptr, 0, sizeof(int), h->stream));
+  k_seg_fill<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, cb.row_vstart, m, cb.vptr, cb.vrow);
+  CK(cudaGetLastError());
+}
+
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   PhaseTimer pt;
   CK(cudaSetDevice(h->device));
@@ -489,7 +530,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->v = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->ps0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->pbar0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
-  h->Lacc = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b, h->stream);
   h->scratch_m = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
@@ -556,6 +596,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     build_csr(h, cb.s0, cb.s1, cb.row_ptr, cb.col_idx, nullptr);
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
     CK(cudaGetLastError());
+    segment_block(h, h->blocks.back());
   }
   CK(cudaStreamSynchronize(h->stream));
   pt.mark("create: device CSR build");
@@ -565,18 +606,25 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
-  int64_t max_bs = 0;
-  for (const ColBlock& cb : h->blocks) max_bs = std::max(max_bs, cb.s1 - cb.s0);
-  const long long tiles1 = (max_bs + 31) / 32, tiles2 = (m + 31) / 32;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_gather, kThreads, 0));
+  int occ3 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<EP_FUSED>, kThreads, 0));
+  int64_t max_bs = 0, max_nv = 0;
+  for (const ColBlock& cb : h->blocks) {
+    max_bs = std::max(max_bs, cb.s1 - cb.s0);
+    max_nv = std::max(max_nv, cb.nv);
+  }
+  const long long tiles1 = (max_bs + 31) / 32, tiles2 = (max_nv + 31) / 32;
   h->grid1 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ1, 1))));
   h->grid2 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ2, 1))));
+  h->grid3 = static_cast<int>(std::max(
+      1LL, std::min<long long>((m + kThreads - 1) / kThreads, 1LL * sms * std::max(occ3, 1))));
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
-                                  2 * static_cast<size_t>(std::max(h->grid2, h->grid1)),
+                                  2 * static_cast<size_t>(std::max(h->grid3, h->grid1)),
                               b, h->stream);
-  h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid2), b, h->stream);
+  h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid3), b, h->stream);
   h->trace_cap = h->cfg.max_iters / h->cfg.trace_every + 2;
   h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b, h->stream);
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&h->ev_batch[i], cudaEventDisableTiming));
@@ -1185,7 +1233,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
-                             h->Lacc,    h->Lbuf,    h->k1_part,   h->k2_part,    h->scratch_m,
+                             h->Lbuf,    h->k1_part,   h->k2_part,    h->scratch_m,
                              h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
   for (int i = 0; i < 2; ++i) {
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
@@ -1199,10 +1247,11 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
       bufs.push_back(p);
   }
   for (auto& e : h->prof_ev) cudaEventDestroy(e);
-  for (ColBlock& cb : h->blocks) {
-    bufs.push_back(cb.row_ptr);
-    bufs.push_back(cb.col_idx);
-  }
+  for (ColBlock& cb : h->blocks)
+    for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
+                    static_cast<void*>(cb.row_vstart), static_cast<void*>(cb.vptr),
+                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.vpart)})
+      bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {
       if (h->stream)
