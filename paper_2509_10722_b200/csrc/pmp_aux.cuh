@@ -95,15 +95,16 @@ __global__ void k_degree(const int* __restrict__ row_ptr, long long m, int* __re
     deg[l] = row_ptr[l + 1] - row_ptr[l];
 }
 
-// Column-block segmentation of the link-major CSR ("virtual rows"): link l
-// with d entries in the block gets ceil(d / kSeg) segments of near-equal
-// size.  nseg[l] -> (exclusive scan) row_vstart; then each link writes its
-// segments' CSR starts and its id.
-__global__ void k_seg_count(const int* __restrict__ row_ptr, long long m, int* __restrict__ nseg) {
+// Column-block segmentation of the link-major CSR (k_link_pass): link l
+// with d entries in the block gets max(1, ceil(d / seg)) segments of
+// near-equal size.  nseg[l] -> (exclusive scan) row_vstart; then each link
+// writes its segments' CSR starts and its id.
+__global__ void k_seg_count(const int* __restrict__ row_ptr, long long m, int seg,
+                            int* __restrict__ nseg) {
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
        l += (long long)gridDim.x * blockDim.x) {
     const int d = row_ptr[l + 1] - row_ptr[l];
-    nseg[l] = (d + kSeg - 1) / kSeg;
+    nseg[l] = max(1, (d + seg - 1) / seg);
   }
 }
 __global__ void k_seg_fill(const int* __restrict__ row_ptr, const int* __restrict__ row_vstart,
@@ -119,12 +120,13 @@ __global__ void k_seg_fill(const int* __restrict__ row_ptr, const int* __restric
     if (l == m - 1) vptr[v0 + ns] = b + d;
   }
 }
-
-// L = combined per-link sums of the preceding k_link_gather launches.
-__global__ void k_link_combine(IterArgs a, double* __restrict__ out) {
-  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < a.m;
+__global__ void k_max_degree(const int* __restrict__ row_ptr, long long m, int* __restrict__ out) {
+  int mx = 0;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
        l += (long long)gridDim.x * blockDim.x)
-    out[l] = combine_link(a, l);
+    mx = max(mx, row_ptr[l + 1] - row_ptr[l]);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
 // warm_start_from (solver.hpp:218-259) in link space, given L = R x0:

@@ -61,7 +61,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
 constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
-constexpr int kSeg = kStageInts / 32;          // max entries per link segment (one staged round per warp)
+constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kMaxBlocks = 16;                 // max column blocks
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -119,9 +119,7 @@ struct IterArgs {
   double* k1_part;  // [nb][grid1][2]: tau dA^2, objective
   double* k2_part;  // [grid2][4]: r^2, dB.dQ, d dB^2, dzs^2
   int grid1, grid2, grid3, nblocks;
-  // per column block: first segment of every link, segment partial sums
-  const int* row_vstart[kMaxBlocks];  // m+1
-  const double* vpart[kMaxBlocks];    // per-segment partials (row tails only)
+  double* Lacc;     // m: link loads accumulated over the column blocks
   double* Lbuf;     // sharded: m partial loads + 2 scalars
   Ctrl* ctrl;
   numpmp_trace_row* trace;
@@ -129,17 +127,19 @@ struct IterArgs {
 };
 
 // One column block: streams [s0, s1), the CSR of their columns, and its
-// segmentation into "virtual rows" of at most kSeg consecutive entries of
-// one link (rows split evenly), so every lane's gather chain is bounded
+// segmentation into segments of at most `seg` consecutive entries of one
+// link (rows split evenly), packed into warp units of <= 32 segments of
+// whole rows (k_link_pass), so every lane's gather chain is bounded
 // whatever the link degree skew.
 struct BlockArgs {
   long long s0, s1;
   const int* col_idx;  // global stream ids, ascending per row
   const int* vptr;     // nv+1: first CSR entry of each segment
   const int* vrow;     // nv: link of each segment
-  double* vpart;       // nv: in-warp partial of the row at its tail segment
-  long long nv;
+  const int* uptr;     // nu+1: first segment of each warp unit
+  long long nv, nu;
   int index;           // block number b
+  int first;           // b == 0
 };
 
 // ---------------------------------------------------------------- helpers
@@ -384,42 +384,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
 }
 
 // --------------------------------------------------------------- K2: links
-// Link-pass gather over one column block: one lane per segment (<= kSeg
-// entries of one link), a warp per 32 consecutive segments (their index
-// span is one staged round).  The segments of a link are adjacent lanes; a
-// fixed-order segmented inclusive scan over the lanes leaves the warp's
-// partial for each link at its last segment in the warp ("tail"), which is
-// stored at vpart[tail].  The epilogue kernel folds the tails of a link
-// (one per warp the link spans, per column block) in a fixed order.
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_gather(IterArgs a, BlockArgs bk,
-                                                                     const double* __restrict__ src) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts];
-  if (a.mode != MODE_AUX && kernel_should_exit(a.ctrl)) return;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol_first = policy_evict_first();
-  const long long nunits = (bk.nv + 31) / 32;
-  for (long long u = (long long)blockIdx.x * kWarps + wib; u < nunits;
-       u += (long long)gridDim.x * kWarps) {
-    const long long v = u * 32 + lane;
-    const bool valid = v < bk.nv;
-    const int vb = __ldg(bk.vptr + (valid ? v : bk.nv));
-    const int ve = valid ? __ldg(bk.vptr + v + 1) : vb;
-    const int row = valid ? __ldg(bk.vrow + v) : -1;
-    const int span_beg = __shfl_sync(kFull, vb, 0);
-    const int span_end = __shfl_sync(kFull, ve, 31);
-    double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
-                                 GatherX{src}, pol_first);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
-      const double t = __shfl_up_sync(kFull, s, d);
-      const int tr = __shfl_up_sync(kFull, row, d);
-      if (lane >= d && tr == row) s += t;
-    }
-    const int next_row = __shfl_down_sync(kFull, row, 1);
-    if (valid && (lane == 31 || next_row != row)) __stcg(bk.vpart + v, s);
-  }
-}
-
 // Per-link epilogue: slack projection (solver.hpp:368-376), link average
 // (110-126), z update split into B / zs / Q (388-399), price (401-405).
 __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, double L, int d,
@@ -451,20 +415,6 @@ __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, do
   a.Q_out[r] = Qn;
   a.pr_out[r] = prn;
   st_hint_f64(a.v + r, Bn + prn / rho, pol_last);
-}
-
-// L_l = sum over column blocks (in order) of the block's tails for link l
-// (one per 32-segment warp unit the link spans, in order).
-__device__ __forceinline__ double combine_link(const IterArgs& a, long long l) {
-  double L = 0.0;
-  for (int b = 0; b < a.nblocks; ++b) {
-    const int rs = __ldg(a.row_vstart[b] + l), re = __ldg(a.row_vstart[b] + l + 1);
-    if (re <= rs) continue;
-    double Lb = 0.0;
-    for (int k = rs >> 5; k <= (re - 1) >> 5; ++k) Lb += __ldcg(a.vpart[b] + min(re - 1, 32 * k + 31));
-    L += Lb;
-  }
-  return L;
 }
 
 // Finalize one iteration on the device: r, s, then the exact control order
@@ -522,32 +472,93 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
   }
 }
 
-// Link epilogue phases (one thread per link, grid-stride).
-//   EP_FUSED    : combine the blocks' tails, epilogue, residual partials,
-//                 last-block finalize (single GPU).
-//   EP_COMBINE  : sharded: local loads -> Lbuf, the last block folds the
-//                 stream-pass scalars into Lbuf[m], Lbuf[m+1]; NCCL next.
-//   EP_EPILOGUE : sharded: replicated epilogue on the all-reduced Lbuf.
-enum : int { EP_FUSED = 0, EP_COMBINE = 1, EP_EPILOGUE = 2 };
+// The last CTA of a fused link pass: fixed-order sums of the stream-pass
+// and link-pass partials, then finalize_iteration.
+__device__ __forceinline__ void last_block_finalize(const IterArgs& a, double rho, int nparts,
+                                                    bool scalars_in_lbuf) {
+  double tda2, obj;
+  if (scalars_in_lbuf) {
+    tda2 = __ldcg(a.Lbuf + a.m);
+    obj = __ldcg(a.Lbuf + a.m + 1);
+  } else {
+    tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
+    obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
+  }
+  const double r2 = block_sum_array(a.k2_part, nparts, 4, 0);
+  const double cross = block_sum_array(a.k2_part, nparts, 4, 1);
+  const double ddb2 = block_sum_array(a.k2_part, nparts, 4, 2);
+  const double dzs2 = block_sum_array(a.k2_part, nparts, 4, 3);
+  if (threadIdx.x == 0) {
+    finalize_iteration(a, rho, tda2, obj, r2, cross, ddb2, dzs2);
+    a.ctrl->ticket = 0;
+    __threadfence();
+  }
+}
 
+// Link-pass phases (one launch per column block b).
+//   LP_ACC    : b < NB-1: block partial of every link -> Lacc (b = 0 stores,
+//               later blocks add in block order).
+//   LP_FUSED  : last block, single GPU: L = Lacc + partial, link epilogue,
+//               residual partials, last-CTA finalize.
+//   LP_GATHER : last block, sharded: local loads -> Lbuf; the last CTA folds
+//               the stream-pass scalars into Lbuf[m], Lbuf[m+1] (one NCCL
+//               all-reduce carries both).
+//   LP_ROWSUM : last block, outside the iteration: L -> out (R src).
+enum : int { LP_ACC = 0, LP_FUSED = 1, LP_GATHER = 2, LP_ROWSUM = 3 };
+
+// Link-pass gather over one column block's CSR, in "warp units": the rows
+// (links) are cut into segments of <= seg entries (near-equal split; every
+// row has >= 1 segment, possibly empty), and consecutive whole rows are
+// packed into units of <= 32 segments.  A warp takes one unit, one lane per
+// segment; a fixed-order segmented inclusive scan over the lanes leaves the
+// block partial of each row at its last ("tail") lane, which owns the row's
+// epilogue.  Rows never cross units, so no second combine pass exists.
 template <int kPhase>
-__global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
+                                                                   const double* __restrict__ src,
+                                                                   double* __restrict__ out) {
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   __shared__ bool s_last;
-  if (kernel_should_exit(a.ctrl)) return;
-  const double rho = a.ctrl->rho;
+  if (a.mode != MODE_AUX && kernel_should_exit(a.ctrl)) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
+  const double rho = (kPhase == LP_FUSED) ? a.ctrl->rho : 0.0;
   double part[4] = {0.0, 0.0, 0.0, 0.0};
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.m;
-       r += (long long)gridDim.x * blockDim.x) {
-    if (kPhase == EP_COMBINE) {
-      a.Lbuf[r] = combine_link(a, r);
-      continue;
+  for (long long u = (long long)blockIdx.x * kWarps + wib; u < bk.nu;
+       u += (long long)gridDim.x * kWarps) {
+    const int v0 = __ldg(bk.uptr + u), v1 = __ldg(bk.uptr + u + 1);
+    const int v = v0 + lane;
+    const bool valid = v < v1;
+    const int vb = __ldg(bk.vptr + (valid ? v : v1));
+    const int ve = valid ? __ldg(bk.vptr + v + 1) : vb;
+    const int row = valid ? __ldg(bk.vrow + v) : -1 - lane;
+    const int span_beg = __shfl_sync(kFull, vb, 0);
+    const int span_end = __shfl_sync(kFull, ve, 31);
+    double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
+                                 GatherX{src}, pol_first);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
+      const double t = __shfl_up_sync(kFull, s, d);
+      const int tr = __shfl_up_sync(kFull, row, d);
+      if (lane >= d && tr == row) s += t;
     }
-    const double L = (kPhase == EP_EPILOGUE) ? __ldcg(a.Lbuf + r) : combine_link(a, r);
-    link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
+    const int next_row = __shfl_down_sync(kFull, row, 1);
+    if (!valid || (lane != 31 && next_row == row)) continue;  // not the row's tail
+    const long long r = row;
+    const double L = bk.first ? s : __ldcg(a.Lacc + r) + s;
+    if (kPhase == LP_ACC) {
+      __stcg(a.Lacc + r, L);
+    } else if (kPhase == LP_ROWSUM) {
+      out[r] = L;
+    } else if (kPhase == LP_GATHER) {
+      a.Lbuf[r] = L;
+    } else {
+      link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
+    }
   }
-  if (kPhase == EP_COMBINE) {
+  if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;
+  if (kPhase == LP_GATHER) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket2, 1u) == gridDim.x - 1);
@@ -569,23 +580,28 @@ __global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  double tda2, obj;
-  if (kPhase == EP_EPILOGUE) {
-    tda2 = __ldcg(a.Lbuf + a.m);
-    obj = __ldcg(a.Lbuf + a.m + 1);
-  } else {
-    tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
-    obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
-  }
-  const double r2 = block_sum_array(a.k2_part, a.grid3, 4, 0);
-  const double cross = block_sum_array(a.k2_part, a.grid3, 4, 1);
-  const double ddb2 = block_sum_array(a.k2_part, a.grid3, 4, 2);
-  const double dzs2 = block_sum_array(a.k2_part, a.grid3, 4, 3);
-  if (threadIdx.x == 0) {
-    finalize_iteration(a, rho, tda2, obj, r2, cross, ddb2, dzs2);
-    a.ctrl->ticket = 0;
-    __threadfence();
-  }
+  last_block_finalize(a, rho, gridDim.x, false);
+}
+
+// Sharded: the replicated link epilogue on the all-reduced loads Lbuf (one
+// thread per link), residual partials, last-CTA finalize.
+__global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
+  __shared__ bool s_last;
+  if (kernel_should_exit(a.ctrl)) return;
+  const double rho = a.ctrl->rho;
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last();
+  double part[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.m;
+       r += (long long)gridDim.x * blockDim.x)
+    link_epilogue(a, r, __ldcg(a.Lbuf + r), __ldg(a.deg + r), rho, part, pol_first, pol_last);
+  block_sum_store<4>(part, a.k2_part + 4 * blockIdx.x);
+  __threadfence();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  last_block_finalize(a, rho, gridDim.x, true);
 }
 
 }  // namespace numpmp_dev

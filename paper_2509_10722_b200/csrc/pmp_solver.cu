@@ -140,10 +140,11 @@ struct ColBlock {
   int64_t s0 = 0, s1 = 0, nnz = 0, nv = 0;
   int* row_ptr = nullptr;     // m+1
   int* col_idx = nullptr;     // nnz + pad, global stream ids
-  int* row_vstart = nullptr;  // m+1: first segment of each link
-  int* vptr = nullptr;        // nv+1
-  int* vrow = nullptr;        // nv
-  double* vpart = nullptr;    // nv
+  int* vptr = nullptr;        // nv+1: first CSR entry of each segment
+  int* vrow = nullptr;        // nv: link of each segment
+  int* uptr = nullptr;        // nu+1: first segment of each warp unit
+  int64_t nu = 0;
+  int seg = 0;                // max entries per segment
 };
 
 }  // namespace
@@ -180,6 +181,7 @@ struct numpmp_gpu {
   double* ps0 = nullptr;    // slack flows of an uploaded state
   double* pbar0 = nullptr;  // link averages of an uploaded state
   double* Lbuf = nullptr;   // m + 2
+  double* Lacc = nullptr;   // m: link loads accumulated over the column blocks
   double* k1_part = nullptr;
   double* k2_part = nullptr;
   double* scratch_m = nullptr;
@@ -213,7 +215,7 @@ struct numpmp_gpu {
 
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
-  int launches_per_iteration() const { return 2 * nb() + (sharded ? 2 : 1); }
+  int launches_per_iteration() const { return 2 * nb() + (sharded ? 1 : 0); }
 };
 
 namespace {
@@ -278,10 +280,7 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.grid2 = h->grid2;
   a.grid3 = h->grid3;
   a.nblocks = h->nb();
-  for (int b = 0; b < h->nb(); ++b) {
-    a.row_vstart[b] = h->blocks[static_cast<size_t>(b)].row_vstart;
-    a.vpart[b] = h->blocks[static_cast<size_t>(b)].vpart;
-  }
+  a.Lacc = h->Lacc;
   a.Lbuf = h->Lbuf;
   a.ctrl = h->ctrl;
   a.trace = h->trace_dev;
@@ -297,9 +296,11 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.col_idx = cb.col_idx;
   k.vptr = cb.vptr;
   k.vrow = cb.vrow;
-  k.vpart = cb.vpart;
+  k.uptr = cb.uptr;
   k.nv = cb.nv;
+  k.nu = cb.nu;
   k.index = b;
+  k.first = b == 0;
   return k;
 }
 
@@ -324,21 +325,19 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
     CK(cudaGetLastError());
     mark();
-    k_link_gather<<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x);
+    if (b + 1 < nb)
+      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+    else if (!h->sharded)
+      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+    else
+      k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     CK(cudaGetLastError());
     mark();
   }
-  if (!h->sharded) {
-    k_link_epilogue<EP_FUSED><<<h->grid3, kThreads, 0, h->stream>>>(a);
-    CK(cudaGetLastError());
-    mark();
-  } else {
-    k_link_epilogue<EP_COMBINE><<<h->grid3, kThreads, 0, h->stream>>>(a);
-    CK(cudaGetLastError());
-    mark();
+  if (h->sharded) {
     NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum, h->comm,
                  h->stream));
-    k_link_epilogue<EP_EPILOGUE><<<h->grid3, kThreads, 0, h->stream>>>(a);
+    k_link_epilogue<<<h->grid3, kThreads, 0, h->stream>>>(a);
     CK(cudaGetLastError());
     mark();
   }
@@ -386,11 +385,12 @@ Ctrl read_ctrl(numpmp_gpu* h) {
 void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
   IterArgs a = make_args(h, h->cur, MODE_AUX);
   for (int b = 0; b < h->nb(); ++b) {
-    k_link_gather<<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src);
+    if (b + 1 < h->nb())
+      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, nullptr);
+    else
+      k_link_pass<LP_ROWSUM><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, out);
     CK(cudaGetLastError());
   }
-  k_link_combine<<<h->grid3, kThreads, 0, h->stream>>>(a, out);
-  CK(cudaGetLastError());
   if (h->sharded)
     NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm, h->stream));
 }
@@ -476,33 +476,65 @@ int choose_blocks(int64_t n) {
   return static_cast<int>(std::min<int64_t>(nb, std::max<int64_t>(1, n / 32)));
 }
 
-// Virtual-row segmentation of one column block's CSR (pmp_kernels.cuh).
+// Warp-unit segmentation of one column block's CSR (k_link_pass): the
+// segment bound is kSeg, raised so that the longest row fits one warp unit
+// (32 segments); consecutive whole rows are then packed greedily into units
+// of <= 32 segments (host pass over the per-row segment counts).
 void segment_block(numpmp_gpu* h, ColBlock& cb) {
   const int64_t m = h->m;
-  int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &h->dev_bytes, h->stream);
-  cb.row_vstart = dalloc<int>(static_cast<size_t>(m) + 1, &h->dev_bytes, h->stream);
+  int64_t tmpb = 0;
+  int* dmax = dalloc<int>(1, &tmpb, h->stream);
+  CK(cudaMemsetAsync(dmax, 0, sizeof(int), h->stream));
+  k_max_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, dmax);
+  CK(cudaGetLastError());
+  int maxd = 0;
+  CK(cudaMemcpyAsync(&maxd, dmax, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFreeAsync(dmax, h->stream);
+  cb.seg = std::max(kSeg, (maxd + 31) / 32);
+  int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
+  int* row_vstart = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
   CK(cudaMemsetAsync(nseg + m, 0, sizeof(int), h->stream));
-  k_seg_count<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, nseg);
+  k_seg_count<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, cb.seg, nseg);
   CK(cudaGetLastError());
   size_t temp_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, nseg, cb.row_vstart, static_cast<int>(m + 1),
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, nseg, row_vstart, static_cast<int>(m + 1),
                                    h->stream));
   void* temp = nullptr;
   CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
-  CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nseg, cb.row_vstart, static_cast<int>(m + 1),
+  CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nseg, row_vstart, static_cast<int>(m + 1),
                                    h->stream));
-  int nv = 0;
-  CK(cudaMemcpyAsync(&nv, cb.row_vstart + m, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  std::vector<int> vstart(static_cast<size_t>(m) + 1);
+  CK(cudaMemcpyAsync(vstart.data(), row_vstart, sizeof(int) * (static_cast<size_t>(m) + 1),
+                     cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   cudaFreeAsync(temp, h->stream);
   cudaFreeAsync(nseg, h->stream);
+  const int nv = vstart[static_cast<size_t>(m)];
   cb.nv = nv;
+  // greedy packing of whole rows into units of <= 32 segments
+  std::vector<int> units;
+  units.reserve(static_cast<size_t>(nv / 16 + 2));
+  int ubeg = 0;
+  units.push_back(0);
+  for (int64_t l = 0; l < m; ++l) {
+    const int re = vstart[static_cast<size_t>(l) + 1];
+    if (re - ubeg > 32) {
+      ubeg = vstart[static_cast<size_t>(l)];
+      units.push_back(ubeg);
+    }
+  }
+  units.push_back(nv);
+  cb.nu = static_cast<int64_t>(units.size()) - 1;
+  cb.uptr = dalloc<int>(units.size(), &h->dev_bytes, h->stream);
+  CK(cudaMemcpyAsync(cb.uptr, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice,
+                     h->stream));
   cb.vptr = dalloc<int>(static_cast<size_t>(nv) + 1, &h->dev_bytes, h->stream);
   cb.vrow = dalloc<int>(static_cast<size_t>(nv), &h->dev_bytes, h->stream);
-  cb.vpart = dalloc<double>(static_cast<size_t>(nv), &h->dev_bytes, h->stream);
-  if (nv == 0) CK(cudaMemsetAsync(cb.vptr, 0, sizeof(int), h->stream));
-  k_seg_fill<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, cb.row_vstart, m, cb.vptr, cb.vrow);
+  k_seg_fill<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, row_vstart, m, cb.vptr, cb.vrow);
   CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));  // `units` is host memory
+  cudaFreeAsync(row_vstart, h->stream);
 }
 
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
@@ -531,6 +563,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->ps0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->pbar0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b, h->stream);
+  h->Lacc = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->scratch_m = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->scratch_n = dalloc<double>(static_cast<size_t>(n), b, h->stream);
@@ -606,15 +639,15 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_gather, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
   int occ3 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<EP_FUSED>, kThreads, 0));
-  int64_t max_bs = 0, max_nv = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue, kThreads, 0));
+  int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
-    max_nv = std::max(max_nv, cb.nv);
+    max_nu = std::max(max_nu, cb.nu);
   }
-  const long long tiles1 = (max_bs + 31) / 32, tiles2 = (max_nv + 31) / 32;
+  const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
   h->grid1 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ1, 1))));
   h->grid2 = static_cast<int>(std::max(
@@ -624,7 +657,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
                                   2 * static_cast<size_t>(std::max(h->grid3, h->grid1)),
                               b, h->stream);
-  h->k2_part = dalloc<double>(4 * static_cast<size_t>(h->grid3), b, h->stream);
+  h->k2_part = dalloc<double>(4 * static_cast<size_t>(std::max(h->grid2, h->grid3)), b, h->stream);
   h->trace_cap = h->cfg.max_iters / h->cfg.trace_every + 2;
   h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b, h->stream);
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&h->ev_batch[i], cudaEventDisableTiming));
@@ -1233,7 +1266,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
-                             h->Lbuf,    h->k1_part,   h->k2_part,    h->scratch_m,
+                             h->Lbuf,    h->Lacc,    h->k1_part,   h->k2_part,    h->scratch_m,
                              h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
   for (int i = 0; i < 2; ++i) {
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
@@ -1249,8 +1282,8 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   for (auto& e : h->prof_ev) cudaEventDestroy(e);
   for (ColBlock& cb : h->blocks)
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
-                    static_cast<void*>(cb.row_vstart), static_cast<void*>(cb.vptr),
-                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.vpart)})
+                    static_cast<void*>(cb.uptr), static_cast<void*>(cb.vptr),
+                    static_cast<void*>(cb.vrow)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {
