@@ -54,7 +54,7 @@ namespace numpmp_dev {
 #define NUMPMP_STAGE_INTS 512
 #endif
 #ifndef NUMPMP_GATHER_UNROLL
-#define NUMPMP_GATHER_UNROLL 4
+#define NUMPMP_GATHER_UNROLL 8
 #endif
 constexpr int kWarps = NUMPMP_WARPS;  // warps per block (gather passes)
 constexpr int kThreads = kWarps * 32;
@@ -63,14 +63,6 @@ constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and ro
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kMaxBlocks = 16;                 // max column blocks
-// Index ring (per warp): kRingPieces pieces of kPieceInts indices, each
-// fetched by one TMA bulk copy and completed on its own mbarrier.
-constexpr int kPieceInts = 128;
-constexpr int kRingPieces = 8;
-constexpr int kRingInts = kPieceInts * kRingPieces;
-// An item (tile / unit) may use the ring if its index span, at the worst
-// alignment, touches at most kRingPieces - 1 pieces (>= 1 piece of lookahead).
-constexpr int kRingMaxSpan = kPieceInts * (kRingPieces - 2);
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { ST_RUNNING = -1, ST_CONVERGED = 0, ST_MAXITERS = 1, ST_TIMELIMIT = 2,
@@ -148,13 +140,6 @@ struct BlockArgs {
   long long nv, nu;
   int index;           // block number b
   int first;           // b == 0
-  // static per-warp work ranges (k_stream_pass: 32-stream tiles; k_link_pass:
-  // warp units), balanced by index count; fb*: the range has an item too
-  // long for the index ring and takes the direct staging path.
-  const int* wr1;
-  const unsigned char* fb1;
-  const int* wr2;
-  const unsigned char* fb2;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -222,14 +207,6 @@ struct GatherV {  // v_l (written by the previous link pass)
   const double* __restrict__ v;
   __device__ __forceinline__ double operator()(int l) const { return __ldg(v + l); }
 };
-struct GatherBU {  // v_l recomputed after a rho change / state upload
-  const double* __restrict__ B;
-  const double* __restrict__ pr;
-  double rho;
-  __device__ __forceinline__ double operator()(int l) const {
-    return __ldg(B + l) + __ldg(pr + l) / rho;
-  }
-};
 struct GatherX {  // x_j (written by this iteration's stream pass)
   const double* __restrict__ x;
   __device__ __forceinline__ double operator()(int j) const { return ld_gather_f64(x + j); }
@@ -272,18 +249,17 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
       if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
     }
     const int lo = max(seg_beg, cb), hi = min(seg_end, c1);
-    int k = lo;
-    for (; k + kUnroll <= hi; k += kUnroll) {
-      int ii[kUnroll];
+    // Batches of kUnroll gathers, the last one predicated: a lane never has
+    // fewer than min(kUnroll, remaining) gathers in flight (the passes are
+    // bound by outstanding L1->L2 requests, not by instructions).
+    for (int k = lo; k < hi; k += kUnroll) {
       double vv[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) ii[u] = sidx[k + u - cb];
+      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + u < hi) ? g(sidx[k + u - cb]) : 0.0;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) vv[u] = g(ii[u]);
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) acc += vv[u];
+      for (int u = 0; u < kUnroll; ++u)
+        if (k + u < hi) acc += vv[u];
     }
-    for (; k < hi; ++k) acc += g(sidx[k - cb]);
     __syncwarp();
     cb = nb;
   }
@@ -338,257 +314,70 @@ __device__ __forceinline__ bool kernel_should_exit(const Ctrl* ctrl) {
   return *reinterpret_cast<const volatile int*>(&ctrl->done) != 0;
 }
 
-// ------------------------------------------------------- warp index ring
-// A warp owns a static, contiguous range of work items whose index spans are
-// contiguous and increasing (32-stream tiles of the CSC, or warp units of
-// the CSR).  The range's index stream [start, end) is fetched into a ring of
-// kRingPieces x kPieceInts ints in shared memory by TMA bulk copies
-// (cp.async.bulk, one elected lane, completion on one mbarrier per piece),
-// up to kRingPieces pieces ahead of the consumer.  The indices never pass
-// through registers or the LSU on the way in, and the fetch of the next
-// items' indices overlaps the gathers of the current one.
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-struct WarpRing {
-  uint32_t sbuf;  // shared-memory address of the ring
-  uint32_t sbar;  // shared-memory address of the kRingPieces mbarriers
-  const int* src;
-  int base;       // absolute index of piece 0 (16-byte aligned)
-  int npieces, issued, ready, released;
-
-  __device__ __forceinline__ void init_barriers(int lane) {
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < kRingPieces; ++k)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar + 8 * k));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-  }
-  __device__ __forceinline__ void start(const int* s, int first, int last, int lane) {
-    src = s;
-    base = first & ~3;
-    npieces = last > first ? (last - base + kPieceInts - 1) / kPieceInts : 0;
-    issued = ready = released = 0;
-    top_up(lane);
-  }
-  __device__ __forceinline__ void issue(int k, int lane) {
-    if (lane == 0) {
-      const uint32_t b = sbar + 8 * (k & (kRingPieces - 1));
-      const uint32_t dst = sbuf + 4 * kPieceInts * (k & (kRingPieces - 1));
-      const int* g = src + base + static_cast<long long>(k) * kPieceInts;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
-                   "r"(kPieceInts * 4)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              dst),
-          "l"(g), "r"(kPieceInts * 4), "r"(b)
-          : "memory");
-    }
-  }
-  __device__ __forceinline__ void top_up(int lane) {
-    while (issued < npieces && issued < released + kRingPieces) {
-      issue(issued, lane);
-      ++issued;
-    }
-  }
-  // Make every piece up to absolute position last-1 resident.
-  __device__ __forceinline__ void acquire(int last) {
-    const int ke = (last - 1 - base) / kPieceInts;
-    if (ke >= issued) __trap();  // item longer than the ring: a host planning bug, never a hang
-    while (ready <= ke) {
-      const uint32_t b = sbar + 8 * (ready & (kRingPieces - 1));
-      const uint32_t par = (ready / kRingPieces) & 1;
-      uint32_t done = 0;
-      while (!done)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(b), "r"(par)
-            : "memory");
-      ++ready;
-    }
-  }
-  // The next item starts at absolute position pos: recycle the pieces
-  // wholly below it (only pieces already waited on).
-  __device__ __forceinline__ void release_below(int pos, int lane) {
-    const int kn = min((pos - base) / kPieceInts, ready);
-    if (kn > released) {
-      __syncwarp();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      released = kn;
-      top_up(lane);
-    }
-  }
-  __device__ __forceinline__ int at(int p) const {
-    int v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(sbuf + 4 * ((p - base) & (kRingInts - 1))));
-    return v;
-  }
-};
-
-// Sum of g over the ring positions [b, e), in index order, kUnroll in flight.
-template <class G>
-__device__ __forceinline__ double ring_segment_sum(const WarpRing& ring, int b, int e, G g) {
-  double acc = 0.0;
-  int k = b;
-  for (; k + kUnroll <= e; k += kUnroll) {
-    int ii[kUnroll];
-    double vv[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) ii[u] = ring.at(k + u);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) vv[u] = g(ii[u]);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) acc += vv[u];
-  }
-  for (; k < e; ++k) acc += g(ring.at(k));
-  return acc;
+// v = B + price / rho is stale after a rho change or a state upload
+// (rho_changed, set by finalize_iteration / the host): recompute it before
+// the iteration's first stream pass.  Exits at entry otherwise.
+__global__ void __launch_bounds__(kThreads) k_refresh_v(IterArgs a) {
+  if (kernel_should_exit(a.ctrl) || a.ctrl->rho_changed == 0) return;
+  const double rho = a.ctrl->rho;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < a.m;
+       l += (long long)gridDim.x * blockDim.x)
+    a.v[l] = a.B_in[l] + a.pr_in[l] / rho;
 }
 
 // ------------------------------------------------------------ K1: streams
 // R^T v gather over the CSC + prox + A update (solver.hpp:325-366
-// restated), for the streams of one column block.  A warp takes its static
-// range of 32-stream tiles [tlo, thi), one lane per stream.
-
-struct TileMeta {  // one lane's stream of a tile
-  int beg, end, kd;
-  double A, w;
-  bool valid;
-};
-__device__ __forceinline__ TileMeta load_tile(const IterArgs& a, const BlockArgs& bk, long long t,
-                                              int lane, uint64_t pol_first) {
-  TileMeta m;
-  const long long j = bk.s0 + 32 * t + lane;
-  m.valid = j < bk.s1;
-  m.beg = __ldg(a.col_ptr + (m.valid ? j : bk.s1));
-  m.end = m.valid ? __ldg(a.col_ptr + j + 1) : m.beg;
-  m.A = 0.0;
-  m.w = 0.0;
-  m.kd = 0;
-  if (m.valid) {
-    m.A = ld_stream_f64(a.A_in + j, pol_first);
-    m.w = __ldg(a.w + j);
-    m.kd = __ldg(a.kind + j);
-  }
-  return m;
-}
-
-__device__ __forceinline__ void stream_update(const IterArgs& a, long long j, const TileMeta& m,
-                                              double sum, double rho, bool trace_it,
-                                              double& p_tda2, double& p_obj, uint64_t pol_first,
-                                              uint64_t pol_last) {
-  const int tau = m.end - m.beg;
-  const double zeta = static_cast<double>(tau) * m.A - sum;
-  const double x = (m.kd == NUMPMP_KIND_LOG) ? prox_log(zeta, m.w, rho, tau)
-                                             : prox_linear_nonneg(zeta, m.w, rho, tau);
-  const double An = a.alpha * x + (1.0 - a.alpha) * m.A;
-  const double dA = An - m.A;
-  st_hint_f64(a.x + j, x, pol_last);
-  st_hint_f64(a.A_out + j, An, pol_first);
-  p_tda2 += static_cast<double>(tau) * dA * dA;
-  if (trace_it) p_obj += (m.kd == NUMPMP_KIND_LOG) ? m.w * log(x) : m.w * x;
-}
-
-// Ring path: the tiles' indices arrive through the warp's TMA ring; the next
-// tile's offsets are loaded while this tile gathers (the stream state is
-// needed only after the gather, so it is issued at the tile's start).
+// restated), for the streams of one column block.
 template <class G>
-__device__ __forceinline__ void stream_pass_ring(const IterArgs& a, const BlockArgs& bk, G g,
-                                                 double rho, bool trace_it, WarpRing& ring,
-                                                 int lane, int tlo, int thi, double& p_tda2,
-                                                 double& p_obj) {
+__device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockArgs& bk, G g,
+                                                 double rho, bool trace_it, int* sidx,
+                                                 double& p_tda2, double& p_obj) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
-  const long long jf = bk.s0 + 32LL * tlo, jl = min(bk.s0 + 32LL * thi, bk.s1);
-  ring.start(a.row_idx, __ldg(a.col_ptr + jf), __ldg(a.col_ptr + jl), lane);
-  long long j = jf + lane;
-  int beg = __ldg(a.col_ptr + min(j, bk.s1));
-  int end = (j < bk.s1) ? __ldg(a.col_ptr + j + 1) : beg;
-  for (int t = tlo; t < thi; ++t, j += 32) {
+  const long long ntiles = (bk.s1 - bk.s0 + 31) / 32;
+  const double alpha = a.alpha;
+  for (long long tile = (long long)blockIdx.x * kWarps + wib; tile < ntiles;
+       tile += (long long)gridDim.x * kWarps) {
+    const long long j = bk.s0 + tile * 32 + lane;
     const bool valid = j < bk.s1;
-    TileMeta cur;
-    cur.valid = valid;
-    cur.beg = beg;
-    cur.end = end;
-    cur.A = 0.0;
-    cur.w = 0.0;
-    cur.kd = 0;
+    const int beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
+    const int end = valid ? __ldg(a.col_ptr + j + 1) : beg;
+    double A = 0.0, w = 0.0;
+    int kd = 0;
+    if (valid) {  // independent of the gather: issue early
+      A = ld_stream_f64(a.A_in + j, pol_first);
+      w = __ldg(a.w + j);
+      kd = __ldg(a.kind + j);
+    }
+    const int span_beg = __shfl_sync(kFull, beg, 0);
+    const int span_end = __shfl_sync(kFull, end, 31);
+    const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
+                                         pol_first);
     if (valid) {
-      cur.A = ld_stream_f64(a.A_in + j, pol_first);
-      cur.w = __ldg(a.w + j);
-      cur.kd = __ldg(a.kind + j);
+      const int tau = end - beg;
+      const double zeta = static_cast<double>(tau) * A - sum;
+      const double x = (kd == NUMPMP_KIND_LOG) ? prox_log(zeta, w, rho, tau)
+                                               : prox_linear_nonneg(zeta, w, rho, tau);
+      const double An = alpha * x + (1.0 - alpha) * A;
+      const double dA = An - A;
+      st_hint_f64(a.x + j, x, pol_last);
+      st_hint_f64(a.A_out + j, An, pol_first);
+      p_tda2 += static_cast<double>(tau) * dA * dA;
+      if (trace_it) p_obj += (kd == NUMPMP_KIND_LOG) ? w * log(x) : w * x;
     }
-    if (t + 1 < thi) {  // next tile's offsets
-      const long long jn = j + 32;
-      beg = __ldg(a.col_ptr + min(jn, bk.s1));
-      end = (jn < bk.s1) ? __ldg(a.col_ptr + jn + 1) : beg;
-    }
-    const int span_beg = __shfl_sync(kFull, cur.beg, 0);
-    const int span_end = __shfl_sync(kFull, cur.end, 31);
-    double sum = 0.0;
-    if (span_end > span_beg) {
-      ring.acquire(span_end);
-      sum = ring_segment_sum(ring, cur.beg, cur.end, g);
-    }
-    ring.release_below(span_end, lane);
-    if (valid) stream_update(a, j, cur, sum, rho, trace_it, p_tda2, p_obj, pol_first, pol_last);
-  }
-}
-
-// Direct path (a tile too long for the ring): indices staged through
-// registers into shared memory, round by round (warp_segments_sum).
-template <class G>
-__device__ __forceinline__ void stream_pass_direct(const IterArgs& a, const BlockArgs& bk, G g,
-                                                   double rho, bool trace_it, int* sidx, int lane,
-                                                   int tlo, int thi, double& p_tda2,
-                                                   double& p_obj) {
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_last = policy_evict_last();
-  for (int t = tlo; t < thi; ++t) {
-    const TileMeta cur = load_tile(a, bk, t, lane, pol_first);
-    const int span_beg = __shfl_sync(kFull, cur.beg, 0);
-    const int span_end = __shfl_sync(kFull, cur.end, 31);
-    const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, cur.beg, cur.end, sidx,
-                                         lane, g, pol_first);
-    if (cur.valid)
-      stream_update(a, bk.s0 + 32LL * t + lane, cur, sum, rho, trace_it, p_tda2, p_obj, pol_first,
-                    pol_last);
   }
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
-  __shared__ __align__(128) int sbuf[kWarps][kRingInts];
-  __shared__ __align__(8) uint64_t sbar[kWarps][kRingPieces];
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const double rho = a.ctrl->rho;
-  const bool rc = a.ctrl->rho_changed != 0;
   const long long k = a.ctrl->run_k + 1;
   const bool trace_it = (a.mode == MODE_RUN) && (k % a.trace_every == 0);
   double part[2] = {0.0, 0.0};
-  const int gw = blockIdx.x * kWarps + wib;
-  const int tlo = __ldg(bk.wr1 + gw), thi = __ldg(bk.wr1 + gw + 1);
-  if (tlo < thi) {
-    // v = B + price / rho is stale after a rho change or a state upload (one
-    // iteration in rho_update_interval): that iteration gathers B and price
-    // directly, on the staging path.
-    if (rc) {
-      stream_pass_direct(a, bk, GatherBU{a.B_in, a.pr_in, rho}, rho, trace_it, sbuf[wib], lane, tlo,
-                         thi, part[0], part[1]);
-    } else if (__ldg(bk.fb1 + gw)) {
-      stream_pass_direct(a, bk, GatherV{a.v}, rho, trace_it, sbuf[wib], lane, tlo, thi, part[0],
-                         part[1]);
-    } else {
-      WarpRing ring;
-      ring.sbuf = smem_addr(sbuf[wib]);
-      ring.sbar = smem_addr(sbar[wib]);
-      ring.init_barriers(lane);
-      stream_pass_ring(a, bk, GatherV{a.v}, rho, trace_it, ring, lane, tlo, thi, part[0], part[1]);
-    }
-  }
+  int* sb = sidx[threadIdx.x >> 5];
+  stream_pass_body(a, bk, GatherV{a.v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 
@@ -718,139 +507,52 @@ enum : int { LP_ACC = 0, LP_FUSED = 1, LP_GATHER = 2, LP_ROWSUM = 3 };
 // Link-pass gather over one column block's CSR, in "warp units": the rows
 // (links) are cut into segments of <= seg entries (near-equal split; every
 // row has >= 1 segment, possibly empty), and consecutive whole rows are
-// packed into units of <= 32 segments.  A warp takes its static range of
-// units, one lane per segment; a fixed-order segmented inclusive scan over
-// the lanes leaves the block partial of each row at its last ("tail") lane,
-// which owns the row's epilogue.  Rows never cross units, so no second
-// combine pass exists.
-
-struct UnitMeta {  // one lane's segment of a unit
-  int vb, ve, row;
-  bool valid;
-};
-// uptr values of units ubase.. are held one per lane in `up`.
-__device__ __forceinline__ UnitMeta load_unit(const BlockArgs& bk, int up, int rel, int lane) {
-  UnitMeta m;
-  const int v0 = __shfl_sync(kFull, up, rel), v1 = __shfl_sync(kFull, up, rel + 1);
-  const int v = v0 + lane;
-  m.valid = v < v1;
-  m.vb = __ldg(bk.vptr + (m.valid ? v : v1));
-  m.ve = m.valid ? __ldg(bk.vptr + v + 1) : m.vb;
-  m.row = m.valid ? __ldg(bk.vrow + v) : -1 - lane;
-  return m;
-}
-
-// Segmented scan of the lanes' partials (segments = equal rows) and the
-// row's action at its tail lane.  Lprev: the row's accumulated load of the
-// earlier column blocks (prefetched; ignored for the first block).
-template <int kPhase>
-__device__ __forceinline__ void unit_finish(const IterArgs& a, const BlockArgs& bk, double s,
-                                            const UnitMeta& m, double Lprev, double* out, int lane,
-                                            double rho, double (&part)[4], uint64_t pol_first,
-                                            uint64_t pol_last) {
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const double t = __shfl_up_sync(kFull, s, d);
-    const int tr = __shfl_up_sync(kFull, m.row, d);
-    if (lane >= d && tr == m.row) s += t;
-  }
-  const int next_row = __shfl_down_sync(kFull, m.row, 1);
-  if (!m.valid || (lane != 31 && next_row == m.row)) return;  // not the row's tail
-  const long long r = m.row;
-  const double L = bk.first ? s : Lprev + s;
-  if (kPhase == LP_ACC) {
-    __stcg(a.Lacc + r, L);
-  } else if (kPhase == LP_ROWSUM) {
-    out[r] = L;
-  } else if (kPhase == LP_GATHER) {
-    a.Lbuf[r] = L;
-  } else {
-    link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
-  }
-}
-
-template <int kPhase>
-__device__ __forceinline__ void link_pass_ring(const IterArgs& a, const BlockArgs& bk,
-                                               const double* __restrict__ src, double* out,
-                                               WarpRing& ring, int lane, int ulo, int uhi,
-                                               double rho, double (&part)[4]) {
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_last = policy_evict_last();
-  int ubase = ulo;
-  int up = __ldg(bk.uptr + min(ubase + lane, uhi));
-  const int sf = __shfl_sync(kFull, up, 0);
-  ring.start(bk.col_idx, __ldg(bk.vptr + sf), __ldg(bk.vptr + __ldg(bk.uptr + uhi)), lane);
-  UnitMeta cur = load_unit(bk, up, 0, lane);
-  double Lcur = 0.0;
-  if (!bk.first && cur.valid) Lcur = __ldcg(a.Lacc + cur.row);
-  for (int u = ulo; u < uhi; ++u) {
-    UnitMeta nxt;
-    nxt.valid = false;
-    nxt.row = -1 - lane;
-    if (u + 1 < uhi) {
-      if (u + 1 - ubase >= 31) {
-        ubase = u + 1;
-        up = __ldg(bk.uptr + min(ubase + lane, uhi));
-      }
-      nxt = load_unit(bk, up, u + 1 - ubase, lane);
-    }
-    const int span_beg = __shfl_sync(kFull, cur.vb, 0);
-    const int span_end = __shfl_sync(kFull, cur.ve, 31);
-    double s = 0.0;
-    if (span_end > span_beg) {
-      ring.acquire(span_end);
-      s = ring_segment_sum(ring, cur.vb, cur.ve, GatherX{src});
-    }
-    ring.release_below(span_end, lane);
-    double Lnxt = 0.0;
-    if (!bk.first && nxt.valid) Lnxt = __ldcg(a.Lacc + nxt.row);
-    unit_finish<kPhase>(a, bk, s, cur, Lcur, out, lane, rho, part, pol_first, pol_last);
-    cur = nxt;
-    Lcur = Lnxt;
-  }
-}
-
-template <int kPhase>
-__device__ __forceinline__ void link_pass_direct(const IterArgs& a, const BlockArgs& bk,
-                                                 const double* __restrict__ src, double* out,
-                                                 int* sidx, int lane, int ulo, int uhi, double rho,
-                                                 double (&part)[4]) {
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_last = policy_evict_last();
-  for (int u = ulo; u < uhi; ++u) {
-    const int up = __ldg(bk.uptr + min(u + lane, uhi));
-    const UnitMeta cur = load_unit(bk, up, 0, lane);
-    const int span_beg = __shfl_sync(kFull, cur.vb, 0);
-    const int span_end = __shfl_sync(kFull, cur.ve, 31);
-    const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, cur.vb, cur.ve, sidx, lane,
-                                       GatherX{src}, pol_first);
-    const double Lprev = (!bk.first && cur.valid) ? __ldcg(a.Lacc + cur.row) : 0.0;
-    unit_finish<kPhase>(a, bk, s, cur, Lprev, out, lane, rho, part, pol_first, pol_last);
-  }
-}
-
+// packed into units of <= 32 segments.  A warp takes one unit, one lane per
+// segment; a fixed-order segmented inclusive scan over the lanes leaves the
+// block partial of each row at its last ("tail") lane, which owns the row's
+// epilogue.  Rows never cross units, so no second combine pass exists.
 template <int kPhase>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
-  __shared__ __align__(128) int sbuf[kWarps][kRingInts];
-  __shared__ __align__(8) uint64_t sbar[kWarps][kRingPieces];
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   __shared__ bool s_last;
   if (a.mode != MODE_AUX && kernel_should_exit(a.ctrl)) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last();
   const double rho = (kPhase == LP_FUSED) ? a.ctrl->rho : 0.0;
   double part[4] = {0.0, 0.0, 0.0, 0.0};
-  const int gw = blockIdx.x * kWarps + wib;
-  const int ulo = __ldg(bk.wr2 + gw), uhi = __ldg(bk.wr2 + gw + 1);
-  if (ulo < uhi) {
-    if (__ldg(bk.fb2 + gw)) {
-      link_pass_direct<kPhase>(a, bk, src, out, sbuf[wib], lane, ulo, uhi, rho, part);
+  for (long long u = (long long)blockIdx.x * kWarps + wib; u < bk.nu;
+       u += (long long)gridDim.x * kWarps) {
+    const int v0 = __ldg(bk.uptr + u), v1 = __ldg(bk.uptr + u + 1);
+    const int v = v0 + lane;
+    const bool valid = v < v1;
+    const int vb = __ldg(bk.vptr + (valid ? v : v1));
+    const int ve = valid ? __ldg(bk.vptr + v + 1) : vb;
+    const int row = valid ? __ldg(bk.vrow + v) : -1 - lane;
+    const int span_beg = __shfl_sync(kFull, vb, 0);
+    const int span_end = __shfl_sync(kFull, ve, 31);
+    double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
+                                 GatherX{src}, pol_first);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
+      const double t = __shfl_up_sync(kFull, s, d);
+      const int tr = __shfl_up_sync(kFull, row, d);
+      if (lane >= d && tr == row) s += t;
+    }
+    const int next_row = __shfl_down_sync(kFull, row, 1);
+    if (!valid || (lane != 31 && next_row == row)) continue;  // not the row's tail
+    const long long r = row;
+    const double L = bk.first ? s : __ldcg(a.Lacc + r) + s;
+    if (kPhase == LP_ACC) {
+      __stcg(a.Lacc + r, L);
+    } else if (kPhase == LP_ROWSUM) {
+      out[r] = L;
+    } else if (kPhase == LP_GATHER) {
+      a.Lbuf[r] = L;
     } else {
-      WarpRing ring;
-      ring.sbuf = smem_addr(sbuf[wib]);
-      ring.sbar = smem_addr(sbar[wib]);
-      ring.init_barriers(lane);
-      link_pass_ring<kPhase>(a, bk, src, out, ring, lane, ulo, uhi, rho, part);
+      link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
     }
   }
   if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;

@@ -31,7 +31,7 @@ using namespace numpmp_dev;
 namespace {
 
 constexpr int kBatchIters = 32;  // iterations per CUDA-graph launch (even)
-constexpr int kIdxPad = 256;     // int32 padding after index arrays (int4 / ring-piece over-read)
+constexpr int kIdxPad = 64;      // int32 padding after index arrays (int4 over-read)
 
 struct GpuError {
   int code;
@@ -145,11 +145,6 @@ struct ColBlock {
   int* uptr = nullptr;        // nu+1: first segment of each warp unit
   int64_t nu = 0;
   int seg = 0;                // max entries per segment
-  std::vector<int64_t> unit_pos;  // host, nu+1: first CSR entry of each unit (work planning)
-  int* wr1 = nullptr;             // per-warp tile ranges of k_stream_pass (grid1*kWarps+1)
-  unsigned char* fb1 = nullptr;   // per-warp direct-path flags
-  int* wr2 = nullptr;             // per-warp unit ranges of k_link_pass (grid2*kWarps+1)
-  unsigned char* fb2 = nullptr;
 };
 
 }  // namespace
@@ -220,7 +215,7 @@ struct numpmp_gpu {
 
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
-  int launches_per_iteration() const { return 2 * nb() + (sharded ? 1 : 0); }
+  int launches_per_iteration() const { return 1 + 2 * nb() + (sharded ? 1 : 0); }
 };
 
 namespace {
@@ -306,10 +301,6 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.nu = cb.nu;
   k.index = b;
   k.first = b == 0;
-  k.wr1 = cb.wr1;
-  k.fb1 = cb.fb1;
-  k.wr2 = cb.wr2;
-  k.fb2 = cb.fb2;
   return k;
 }
 
@@ -329,6 +320,9 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
   if (record_first) mark();
   else ++e;
   const int nb = h->nb();
+  k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
+  CK(cudaGetLastError());
+  mark();
   for (int b = 0; b < nb; ++b) {
     const BlockArgs bk = block_args(h, b);
     k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
@@ -522,30 +516,18 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   const int nv = vstart[static_cast<size_t>(m)];
   cb.nv = nv;
   // greedy packing of whole rows into units of <= 32 segments
-  std::vector<int> units, urow;
+  std::vector<int> units;
   units.reserve(static_cast<size_t>(nv / 16 + 2));
-  urow.reserve(static_cast<size_t>(nv / 16 + 2));
   int ubeg = 0;
   units.push_back(0);
-  urow.push_back(0);
   for (int64_t l = 0; l < m; ++l) {
     const int re = vstart[static_cast<size_t>(l) + 1];
     if (re - ubeg > 32) {
       ubeg = vstart[static_cast<size_t>(l)];
       units.push_back(ubeg);
-      urow.push_back(static_cast<int>(l));
     }
   }
   units.push_back(nv);
-  urow.push_back(static_cast<int>(m));
-  {
-    std::vector<int> rp(static_cast<size_t>(m) + 1);
-    CK(cudaMemcpyAsync(rp.data(), cb.row_ptr, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost,
-                       h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cb.unit_pos.resize(urow.size());
-    for (size_t u = 0; u < urow.size(); ++u) cb.unit_pos[u] = rp[static_cast<size_t>(urow[u])];
-  }
   cb.nu = static_cast<int64_t>(units.size()) - 1;
   cb.uptr = dalloc<int>(units.size(), &h->dev_bytes, h->stream);
   CK(cudaMemcpyAsync(cb.uptr, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice,
@@ -556,36 +538,6 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));  // `units` is host memory
   cudaFreeAsync(row_vstart, h->stream);
-}
-
-// Static per-warp work ranges: items i = 0..N-1 with index spans
-// [pos[i], pos[i+1]) are cut into nw contiguous ranges of near-equal cost
-// (span + per-item overhead).  A range that holds an item longer than the
-// index ring allows takes the direct path.
-void plan_warps(numpmp_gpu* h, const std::vector<int64_t>& pos, int nw, int64_t item_cost,
-                int** wr_out, unsigned char** fb_out) {
-  const int64_t N = static_cast<int64_t>(pos.size()) - 1;
-  std::vector<int> wr(static_cast<size_t>(nw) + 1);
-  std::vector<unsigned char> fb(static_cast<size_t>(nw), 0);
-  auto cum = [&](int64_t i) { return (pos[static_cast<size_t>(i)] - pos[0]) + item_cost * i; };
-  const double total = static_cast<double>(cum(N));
-  int64_t i = 0;
-  for (int w = 0; w <= nw; ++w) {
-    const double target = total * static_cast<double>(w) / nw;
-    while (i < N && static_cast<double>(cum(i)) < target) ++i;
-    wr[static_cast<size_t>(w)] = static_cast<int>(w == nw ? N : i);
-  }
-  for (int w = 0; w < nw; ++w)
-    for (int64_t t = wr[static_cast<size_t>(w)]; t < wr[static_cast<size_t>(w) + 1]; ++t)
-      if (pos[static_cast<size_t>(t) + 1] - pos[static_cast<size_t>(t)] > kRingMaxSpan) {
-        fb[static_cast<size_t>(w)] = 1;
-        break;
-      }
-  *wr_out = dalloc<int>(wr.size(), &h->dev_bytes, h->stream);
-  *fb_out = dalloc<unsigned char>(fb.size(), &h->dev_bytes, h->stream);
-  CK(cudaMemcpyAsync(*wr_out, wr.data(), sizeof(int) * wr.size(), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemcpyAsync(*fb_out, fb.data(), fb.size(), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaStreamSynchronize(h->stream));  // host vectors go out of scope
 }
 
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
@@ -705,15 +657,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
       1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ2, 1))));
   h->grid3 = static_cast<int>(std::max(
       1LL, std::min<long long>((m + kThreads - 1) / kThreads, 1LL * sms * std::max(occ3, 1))));
-  for (ColBlock& cb : h->blocks) {
-    const int64_t tiles = (cb.s1 - cb.s0 + 31) / 32;
-    std::vector<int64_t> tpos(static_cast<size_t>(tiles) + 1);
-    for (int64_t t = 0; t <= tiles; ++t)
-      tpos[static_cast<size_t>(t)] = pv->stream_offsets[std::min(cb.s0 + 32 * t, cb.s1)];
-    plan_warps(h, tpos, h->grid1 * kWarps, 32, &cb.wr1, &cb.fb1);
-    plan_warps(h, cb.unit_pos, h->grid2 * kWarps, 32, &cb.wr2, &cb.fb2);
-    std::vector<int64_t>().swap(cb.unit_pos);
-  }
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
                                   2 * static_cast<size_t>(std::max(h->grid3, h->grid1)),
                               b, h->stream);
@@ -732,7 +675,7 @@ void reset_ctrl(numpmp_gpu* h, double rho, int64_t iter) {
   c.iter = iter;
   c.run_k = 0;
   c.status = ST_RUNNING;
-  c.rho_changed = 1;  // the first K1 builds v from B and price
+  c.rho_changed = 1;  // k_refresh_v builds v from B and price
   std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
   CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -1096,9 +1039,9 @@ void run_loop(numpmp_gpu* h) {
         float t = 0.f;
         const size_t e0 = static_cast<size_t>(set) * set_size + static_cast<size_t>(i * lpi + l);
         CK(cudaEventElapsedTime(&t, h->prof_ev[e0], h->prof_ev[e0 + 1]));
-        // launches alternate stream pass / link pass; the sharded
-        // epilogue (last launch) counts as link pass.
-        if ((l & 1) == 0 && l < 2 * h->nb())
+        // launch 0 refreshes v (stream side), then stream pass / link
+        // pass alternate; the sharded epilogue (last launch) is link side.
+        if (l == 0 || ((l & 1) == 1 && l < 2 * h->nb()))
           h->prof_ms_k1 += t;
         else
           h->prof_ms_k2 += t;
@@ -1343,9 +1286,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   for (ColBlock& cb : h->blocks)
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
                     static_cast<void*>(cb.uptr), static_cast<void*>(cb.vptr),
-                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.wr1),
-                    static_cast<void*>(cb.fb1), static_cast<void*>(cb.wr2),
-                    static_cast<void*>(cb.fb2)})
+                    static_cast<void*>(cb.vrow)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {
