@@ -320,19 +320,22 @@ def run_ours(args):
     iter_gbs = (k1b + k2b) / (iter_ms * 1e-3) / 1e9
     # DRAM traffic of the dominant kernel per iteration, from the committed
     # ncu --set full capture (profiles/traffic_r1.json; config C, one GPU)
-    traffic = None
+    traffic, xbar_pct = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic_r1.json")) as f:
             tr = json.load(f)
         if tr.get("config") == name and world == 1:
             key = "k_link_pass" if avg2 >= avg1 else "k_stream_pass"
             traffic = tr["per_iteration"][key]["dram_bytes"]
+            xbar_pct = tr["per_iteration"][key].get("xbar_req_pct")
     except Exception:
         traffic = None
     # The structural bound: one random 8-byte gather per nonzero and pass,
-    # at the measured B200 gather ceiling (scripts/gather_bench.cu,
-    # profiles/r1_gather_microbench.txt: 271 G/s from an L2-resident vector).
-    gather_peak = 271.0e9
+    # each one L1->L2 request; an SM issues at most one such request per
+    # cycle (ncu l1tex__m_l1tex2xbar_req_cycles_active).  Measured ceiling:
+    # scripts/gather_lanes_bench.cu, 269 G gathers/s from an L2-resident
+    # vector at 92.5% of that request rate (profiles/r1_gather_lanes.txt).
+    gather_peak = 269.0e9
     gather_rate = lp.nnz / (dom_ms * 1e-3)
 
     # e2e: the public C-ABI from pinned host buffers, per step:
@@ -407,7 +410,9 @@ def run_ours(args):
                          "launch": "one pass over all column blocks per iteration",
                          "gather_bound": {"achieved_gathers_per_s": gather_rate, "peak_gathers_per_s": gather_peak,
                                           "frac": gather_rate / gather_peak,
-                                          "source": "scripts/gather_bench.cu (profiles/r1_gather_microbench.txt)"}},
+                                          "l1_to_l2_request_pct_ncu": xbar_pct,
+                                          "source": "scripts/gather_lanes_bench.cu (profiles/r1_gather_lanes.txt); "
+                                                    "request utilisation: profiles/traffic_r1.json"}},
             "iteration_roofline": {"alg_bytes": k1b + k2b, "ms": iter_ms, "achieved_gbs": iter_gbs,
                                    "frac": iter_gbs / hbm, "stream_pass_ms": avg1, "link_pass_ms": avg2},
             "gpu_launches": int(launches.value) + args.steps,
