@@ -117,6 +117,29 @@ int numpmp_gpu_create_sharded(const numpmp_problem_view* shard, const numpmp_con
                               int64_t stream_begin, int64_t n_total, numpmp_gpu** out);
 int numpmp_gpu_nccl_unique_id(void* out128);
 
+/* Sharded variant with the fused peer-memory exchange (the default for
+ * multi-GPU runs; pmp_p2p.cuh): links are owned in contiguous ranges, the
+ * link pass stores every row's partial load straight into the owner's HBM
+ * over NVLink, each owner runs the link epilogue for its links and stores
+ * v into every rank's HBM; two system-scope barriers per iteration, no
+ * NCCL kernel in the loop.  Setup, all collective over the ranks:
+ *   numpmp_gpu_create_p2p  -> numpmp_gpu_p2p_export (64-byte CUDA IPC
+ *   handle of the exchange region; the caller all-gathers them) ->
+ *   numpmp_gpu_p2p_connect (rank-ordered world x 64 bytes) ->
+ *   numpmp_gpu_p2p_start (global link degrees / nnz through the exchange).
+ * numpmp_gpu_p2p_connect_local wires `world` handles of one process instead
+ * (one GPU, or several with peer access); each handle must then be driven
+ * by its own host thread, as each rank by its own process.
+ * Every later call that runs iterations or collectives (set_warm, step,
+ * run, run_device) is collective too. */
+int numpmp_gpu_create_p2p(const numpmp_problem_view* shard, const numpmp_config* config,
+                          int device, int rank, int world, int64_t stream_begin, int64_t n_total,
+                          numpmp_gpu** out);
+int numpmp_gpu_p2p_export(numpmp_gpu* h, void* out64);
+int numpmp_gpu_p2p_connect(numpmp_gpu* h, const void* handles);
+int numpmp_gpu_p2p_connect_local(numpmp_gpu** handles, int world);
+int numpmp_gpu_p2p_start(numpmp_gpu* h);
+
 /* Replaces PmpSolver::cold_state (solver.hpp:293-303). */
 int numpmp_gpu_set_cold(numpmp_gpu* h);
 

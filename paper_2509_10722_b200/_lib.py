@@ -108,6 +108,14 @@ SIGNATURES = {
         [C.POINTER(ProblemView), C.POINTER(Config), C.c_int, C.c_int, C.c_int, P, I64, I64, C.POINTER(P)],
     ),
     "numpmp_gpu_nccl_unique_id": (C.c_int, [P]),
+    "numpmp_gpu_create_p2p": (
+        C.c_int,
+        [C.POINTER(ProblemView), C.POINTER(Config), C.c_int, C.c_int, C.c_int, I64, I64, C.POINTER(P)],
+    ),
+    "numpmp_gpu_p2p_export": (C.c_int, [P, P]),
+    "numpmp_gpu_p2p_connect": (C.c_int, [P, P]),
+    "numpmp_gpu_p2p_connect_local": (C.c_int, [C.POINTER(P), C.c_int]),
+    "numpmp_gpu_p2p_start": (C.c_int, [P]),
     "numpmp_gpu_set_cold": (C.c_int, [P]),
     "numpmp_gpu_set_warm": (C.c_int, [P, P, P, D]),
     "numpmp_gpu_set_state": (C.c_int, [P, P, P, P, P, D, I64]),

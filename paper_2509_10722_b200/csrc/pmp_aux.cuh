@@ -234,4 +234,15 @@ __global__ void k_sum_parts(const double* __restrict__ part, int count, double* 
 
 __global__ void k_start_clock(Ctrl* c) { c->t0_ns = globaltimer_ns(); }
 
+__global__ void k_int_to_double(const int* __restrict__ in, long long count, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+__global__ void k_double_to_int(const double* __restrict__ in, long long count, int* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = static_cast<int>(in[i]);
+}
+
 }  // namespace numpmp_dev

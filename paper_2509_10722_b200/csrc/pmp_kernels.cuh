@@ -87,7 +87,27 @@ struct Ctrl {
   int rho_changed;   // next stream pass recomputes v = B + price / rho
   unsigned ticket;   // last-block detection, link pass
   unsigned ticket2;  // last-block detection, sharded gather pass
-  int pad;
+  unsigned ticket3;  // last-block detection, peer-memory owner epilogue
+};
+
+// Peer-memory exchange of the sharded engine (pmp_p2p.cuh).  Links are
+// owned by ranks in contiguous ranges of mo links; every rank maps the
+// exchange regions of all ranks (CUDA IPC / same process), so a kernel
+// stores straight into a peer's HBM over NVLink.
+constexpr int kMaxRanks = 8;
+struct P2PArgs {
+  int rank, world;   // world == 0: not connected
+  long long mo;      // links per owner (ceil(m / world)); owner(l) = l / mo
+  long long l0, l1;  // this rank's links
+  // device-resident tables of `world` peer pointers (index = rank q)
+  double* const* slots_peer;              // rank q's slots: [world][mo] doubles
+  double* const* v_peer;                  // rank q's v: m doubles
+  double* const* xs_peer;                 // rank q's scalar slots: [world][8] doubles
+  unsigned long long* const* flags_peer;  // rank q's barrier counters [4]
+  unsigned long long* flags;                 // local barrier counters [4]
+  unsigned long long* done_cnt;              // local completed-barrier counts [4]
+  double* ep_part;                           // [grid3][4]: owner-epilogue residual partials
+  double* k1_scalars;                        // 2: this rank's stream-pass scalars
 };
 
 struct IterArgs {
@@ -124,6 +144,7 @@ struct IterArgs {
   Ctrl* ctrl;
   numpmp_trace_row* trace;
   long long trace_cap;
+  P2PArgs p2p;
 };
 
 // One column block: streams [s0, s1), the CSR of their columns, and its
@@ -384,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
 // --------------------------------------------------------------- K2: links
 // Per-link epilogue: slack projection (solver.hpp:368-376), link average
 // (110-126), z update split into B / zs / Q (388-399), price (401-405).
-__device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, double L, int d,
+__device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, double L, int d,
                                               double rho, double (&part)[4], uint64_t pol,
                                               uint64_t pol_last) {
   const double alpha = a.alpha;
@@ -412,7 +433,9 @@ __device__ __forceinline__ void link_epilogue(const IterArgs& a, long long r, do
   a.zs_out[r] = zsn;
   a.Q_out[r] = Qn;
   a.pr_out[r] = prn;
-  st_hint_f64(a.v + r, Bn + prn / rho, pol_last);
+  const double vn = Bn + prn / rho;
+  st_hint_f64(a.v + r, vn, pol_last);
+  return vn;
 }
 
 // Finalize one iteration on the device: r, s, then the exact control order
@@ -502,7 +525,23 @@ __device__ __forceinline__ void last_block_finalize(const IterArgs& a, double rh
 //               the stream-pass scalars into Lbuf[m], Lbuf[m+1] (one NCCL
 //               all-reduce carries both).
 //   LP_ROWSUM : last block, outside the iteration: L -> out (R src).
-enum : int { LP_ACC = 0, LP_FUSED = 1, LP_GATHER = 2, LP_ROWSUM = 3 };
+//   LP_P2P    : last block, peer-memory exchange: the row's local load is
+//               stored straight into the owning rank's slot for this rank
+//               (NVLink store, overlapped with the remaining gathers); the
+//               last CTA saves the stream-pass scalars and signals every
+//               rank (pmp_p2p.cuh).
+enum : int { LP_ACC = 0, LP_FUSED = 1, LP_GATHER = 2, LP_ROWSUM = 3, LP_P2P = 4 };
+
+// Read-only load of a pointer from a device-resident table.
+template <class T>
+__device__ __forceinline__ T* ld_ptr(T* const* p) {
+  return reinterpret_cast<T*>(__ldg(reinterpret_cast<const unsigned long long*>(p)));
+}
+
+// System-scope release increment of a (possibly peer) barrier counter.
+__device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
+  asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+}
 
 // Link-pass gather over one column block's CSR, in "warp units": the rows
 // (links) are cut into segments of <= seg entries (near-equal split; every
@@ -551,11 +590,33 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       out[r] = L;
     } else if (kPhase == LP_GATHER) {
       a.Lbuf[r] = L;
+    } else if (kPhase == LP_P2P) {
+      const long long q = r / a.p2p.mo;
+      double* dst = ld_ptr(a.p2p.slots_peer + q);
+      dst[a.p2p.rank * a.p2p.mo + (r - q * a.p2p.mo)] = L;
     } else {
       link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
     }
   }
   if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;
+  if (kPhase == LP_P2P) {
+    __threadfence_system();  // this thread's peer stores, before the ticket
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket2, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence_system();
+    const double tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
+    const double obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
+    if (threadIdx.x == 0) {
+      a.p2p.k1_scalars[0] = tda2;
+      a.p2p.k1_scalars[1] = obj;
+      a.ctrl->ticket2 = 0;
+      __threadfence_system();
+      for (int q = 0; q < a.p2p.world; ++q) signal_sys(a.p2p.flags_peer[q] + 0);  // "loads stored"
+    }
+    return;
+  }
   if (kPhase == LP_GATHER) {
     __threadfence();
     __syncthreads();

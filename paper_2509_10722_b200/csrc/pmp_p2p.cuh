@@ -1,0 +1,215 @@
+// pmp_p2p.cuh -- the sharded engine's peer-memory exchange (one process per
+// GPU on one NVLink/NVSwitch node), fused into the iteration's kernels.
+//
+// streams (columns of R) are sharded, so each rank holds a
+// partial load R_g x_g for every link.  Instead of an all-reduce of the m
+// partial loads followed by a replicated link epilogue on every rank, the
+// links are owned in contiguous ranges of mo = ceil(m / world):
+//
+//   k_link_pass<LP_P2P>  every row's local load goes straight from the tail
+//                        lane into the owner's slot for this rank (an
+//                        NVLink store, overlapped with the remaining
+//                        gathers); the last CTA signals "loads stored".
+//   k_p2p_wait<0>        1 CTA: waits for all ranks' signals (system-scope
+//                        acquire on a local counter).
+//   k_p2p_epilogue       the owner sums its links' slots in rank order (a
+//                        fixed order: deterministic, identical whatever the
+//                        arrival order), runs the link epilogue for its links
+//                        only, stores v_l into every rank's v (NVLink), and
+//                        the last CTA publishes the rank's residual partials
+//                        to every rank and signals "epilogue done".
+//   k_p2p_finalize       1 CTA: waits, sums the ranks' partials in rank
+//                        order -- the same numbers on every rank, so every
+//                        rank takes the same termination / rho decision --
+//                        and runs finalize_iteration.
+//
+// After a rho change v must be rebuilt from B and price, which are current
+// only on the owners: k_p2p_refresh_v (owned links, scattered to every
+// rank) + k_p2p_wait<2> run first in every iteration and exit at entry
+// unless rho_changed.  Traffic per rank and iteration: 8 (world-1)/world
+// bytes per link in each direction, the same as a ring all-reduce, but the
+// epilogue work is divided by world and no NCCL kernel sits in the loop.
+//
+// Ordering (why no buffer is overwritten while it is read): a rank stores
+// into a peer's slots only in k_link_pass(k+1), after its finalize(k) saw
+// every rank's "epilogue done"(k), which each rank signals after reading its
+// slots; v is written in epilogue(k) only after every rank's "loads
+// stored"(k), i.e. after every rank's stream passes of iteration k.
+//
+// Barrier counters are cumulative (flags[i] on the receiving rank, bumped by
+// every rank with red.release.sys); done_cnt[i] counts the barriers of kind
+// i this rank has completed, identical on all ranks because every rank runs
+// the same sequence: target = world * (done_cnt[i] + 1).
+//   flags[0] loads stored / aux push, flags[1] epilogue done / aux result,
+//   flags[2] v refreshed, flags[3] aux buffers free.
+#pragma once
+
+#include "pmp_kernels.cuh"
+
+namespace numpmp_dev {
+
+constexpr long long kP2PTimeoutNs = 60ll * 1000 * 1000 * 1000;  // a dead peer traps, never hangs
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void p2p_wait_counter(const P2PArgs& p, int which) {
+  const unsigned long long target =
+      static_cast<unsigned long long>(p.world) * (p.done_cnt[which] + 1);
+  const long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(p.flags + which) < target) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > kP2PTimeoutNs) __trap();
+  }
+  p.done_cnt[which] += 1;
+  __threadfence();
+}
+
+__device__ __forceinline__ void p2p_signal_all(const P2PArgs& p, int which) {
+  __threadfence_system();
+  for (int q = 0; q < p.world; ++q) signal_sys(ld_ptr(p.flags_peer + q) + which);
+}
+
+// ---------------------------------------------------------------- iteration
+// kCheck: 0 = always wait, 1 = only if rho_changed (the v refresh barrier).
+template <int kWhich, int kOnlyIfRhoChanged>
+__global__ void k_p2p_wait(IterArgs a) {
+  if (threadIdx.x != 0) return;
+  if (kernel_should_exit(a.ctrl)) return;
+  if (kOnlyIfRhoChanged && a.ctrl->rho_changed == 0) return;
+  p2p_wait_counter(a.p2p, kWhich);
+}
+
+__global__ void __launch_bounds__(kThreads) k_p2p_refresh_v(IterArgs a) {
+  __shared__ bool s_last;
+  if (kernel_should_exit(a.ctrl) || a.ctrl->rho_changed == 0) return;
+  const double rho = a.ctrl->rho;
+  const P2PArgs& p = a.p2p;
+  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double v = a.B_in[l] + a.pr_in[l] / rho;
+    for (int q = 0; q < p.world; ++q) ld_ptr(p.v_peer + q)[l] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket3, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  a.ctrl->ticket3 = 0;
+  p2p_signal_all(p, 2);
+}
+
+__global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
+  __shared__ bool s_last;
+  if (kernel_should_exit(a.ctrl)) return;
+  const double rho = a.ctrl->rho;
+  const P2PArgs& p = a.p2p;
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last();
+  double part[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* slots = ld_ptr(p.slots_peer + p.rank);
+  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
+       l += (long long)gridDim.x * blockDim.x) {
+    double L = 0.0;
+    for (int q = 0; q < p.world; ++q) L += __ldcg(slots + q * p.mo + (l - p.l0));
+    const double v = link_epilogue(a, l, L, __ldg(a.deg + l), rho, part, pol_first, pol_last);
+    for (int q = 0; q < p.world; ++q)
+      if (q != p.rank) ld_ptr(p.v_peer + q)[l] = v;
+  }
+  block_sum_store<4>(part, p.ep_part + 4 * blockIdx.x);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket3, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double r2 = block_sum_array(p.ep_part, gridDim.x, 4, 0);
+  const double cross = block_sum_array(p.ep_part, gridDim.x, 4, 1);
+  const double ddb2 = block_sum_array(p.ep_part, gridDim.x, 4, 2);
+  const double dzs2 = block_sum_array(p.ep_part, gridDim.x, 4, 3);
+  if (threadIdx.x == 0) {
+    const double row[6] = {__ldcg(p.k1_scalars), __ldcg(p.k1_scalars + 1), r2, cross, ddb2, dzs2};
+    for (int q = 0; q < p.world; ++q) {
+      double* xs = ld_ptr(p.xs_peer + q) + 8 * p.rank;
+      for (int i = 0; i < 6; ++i) xs[i] = row[i];
+    }
+    a.ctrl->ticket3 = 0;
+    p2p_signal_all(p, 1);
+  }
+}
+
+__global__ void k_p2p_finalize(IterArgs a) {
+  if (threadIdx.x != 0) return;
+  if (kernel_should_exit(a.ctrl)) return;
+  const double rho = a.ctrl->rho;
+  const P2PArgs& p = a.p2p;
+  p2p_wait_counter(p, 1);
+  double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const double* xs = ld_ptr(p.xs_peer + p.rank);
+  for (int q = 0; q < p.world; ++q)
+    for (int i = 0; i < 6; ++i) s[i] += __ldcg(xs + 8 * q + i);
+  finalize_iteration(a, rho, s[0], s[1], s[2], s[3], s[4], s[5]);
+}
+
+// ------------------------------------------------- collectives (setup/post)
+// Used outside the iteration loop (degrees at connect, R x for warm starts
+// and post-processing, the owners' link state after a run).  Each is
+// push -> barrier -> combine -> barrier "buffers free".
+__global__ void k_p2p_aux_wait(P2PArgs p, int which) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) p2p_wait_counter(p, which);
+}
+__global__ void k_p2p_aux_signal(P2PArgs p, int which) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) p2p_signal_all(p, which);
+}
+// src[m] -> owners' slots [rank][local] (reduce layout)
+__global__ void k_p2p_push_partials(P2PArgs p, const double* __restrict__ src, long long m) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const long long q = l / p.mo;
+    ld_ptr(p.slots_peer + q)[p.rank * p.mo + (l - q * p.mo)] = src[l];
+  }
+  __threadfence_system();
+}
+// owner: sum of the ranks' partials (rank order) -> every rank's v
+__global__ void k_p2p_reduce_bcast(P2PArgs p) {
+  const double* slots = ld_ptr(p.slots_peer + p.rank);
+  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
+       l += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < p.world; ++q) s += __ldcg(slots + q * p.mo + (l - p.l0));
+    for (int q = 0; q < p.world; ++q) ld_ptr(p.v_peer + q)[l] = s;
+  }
+  __threadfence_system();
+}
+// owner's links of src -> every rank's slots, global link layout (gather)
+__global__ void k_p2p_push_owned(P2PArgs p, const double* __restrict__ src) {
+  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double x = src[l];
+    for (int q = 0; q < p.world; ++q) ld_ptr(p.slots_peer + q)[l] = x;
+  }
+  __threadfence_system();
+}
+// k scalars of this rank -> every rank's xs row `rank`
+__global__ void k_p2p_push_scalars(P2PArgs p, const double* __restrict__ src, int k) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int q = 0; q < p.world; ++q) {
+    double* xs = ld_ptr(p.xs_peer + q) + 8 * p.rank;
+    for (int i = 0; i < k; ++i) xs[i] = src[i];
+  }
+  __threadfence_system();
+}
+__global__ void k_p2p_sum_scalars(P2PArgs p, double* __restrict__ dst, int k) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const double* xs = ld_ptr(p.xs_peer + p.rank);
+  for (int i = 0; i < k; ++i) {
+    double s = 0.0;
+    for (int q = 0; q < p.world; ++q) s += __ldcg(xs + 8 * q + i);
+    dst[i] = s;
+  }
+}
+
+}  // namespace numpmp_dev

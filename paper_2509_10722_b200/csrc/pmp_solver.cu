@@ -25,6 +25,7 @@
 #include "numpmp_host.h"
 #include "pmp_aux.cuh"
 #include "pmp_kernels.cuh"
+#include "pmp_p2p.cuh"
 
 using namespace numpmp_dev;
 
@@ -159,6 +160,17 @@ struct numpmp_gpu {
   bool sharded = false;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  // peer-memory exchange (pmp_p2p.cuh); xregion = [v | slots | xs | flags],
+  // cudaMalloc'd so that it can be exported with CUDA IPC
+  bool p2p = false;
+  void* xregion = nullptr;
+  size_t xregion_bytes = 0;
+  int64_t mo = 0, l0 = 0, l1 = 0;
+  std::vector<void*> peer_bases;     // opened IPC mappings (closed at destroy)
+  void** peer_tables = nullptr;      // device: 4 tables of world pointers
+  unsigned long long* done_cnt = nullptr;
+  double* ep_part = nullptr;
+  double* k1_scalars = nullptr;
   int64_t dev_bytes = 0;
 
   // problem
@@ -215,7 +227,10 @@ struct numpmp_gpu {
 
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
-  int launches_per_iteration() const { return 1 + 2 * nb() + (sharded ? 1 : 0); }
+  int launches_per_iteration() const {
+    return p2p ? 2 * nb() + 5 : 1 + 2 * nb() + (sharded ? 1 : 0);
+  }
+  std::vector<int> launch_side;  // per launch of an iteration: 1 stream side, 2 link side
 };
 
 namespace {
@@ -239,6 +254,33 @@ const char* validate_config(const numpmp_config* c) {
   if (c->threads < 0) return "threads must be >= 0";
   if (c->time_limit < 0.0) return "time_limit must be >= 0";
   return nullptr;
+}
+
+// Exchange region layout: [v: m][slots: world*mo][xs: world*8] doubles,
+// then [flags: 4] u64.
+size_t xr_slots_off(const numpmp_gpu* h) { return 8 * static_cast<size_t>(h->m); }
+size_t xr_xs_off(const numpmp_gpu* h) {
+  return xr_slots_off(h) + 8 * static_cast<size_t>(h->world) * static_cast<size_t>(h->mo);
+}
+size_t xr_flags_off(const numpmp_gpu* h) { return xr_xs_off(h) + 64 * static_cast<size_t>(h->world); }
+
+P2PArgs p2p_args(const numpmp_gpu* h) {
+  P2PArgs p{};
+  p.rank = h->rank;
+  p.world = h->world;
+  p.mo = h->mo;
+  p.l0 = h->l0;
+  p.l1 = h->l1;
+  const size_t W = static_cast<size_t>(h->world);
+  p.slots_peer = reinterpret_cast<double* const*>(h->peer_tables);
+  p.v_peer = reinterpret_cast<double* const*>(h->peer_tables + W);
+  p.xs_peer = reinterpret_cast<double* const*>(h->peer_tables + 2 * W);
+  p.flags_peer = reinterpret_cast<unsigned long long* const*>(h->peer_tables + 3 * W);
+  p.flags = reinterpret_cast<unsigned long long*>(static_cast<char*>(h->xregion) + xr_flags_off(h));
+  p.done_cnt = h->done_cnt;
+  p.ep_part = h->ep_part;
+  p.k1_scalars = h->k1_scalars;
+  return p;
 }
 
 IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
@@ -285,6 +327,7 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.ctrl = h->ctrl;
   a.trace = h->trace_dev;
   a.trace_cap = h->trace_cap;
+  if (h->p2p) a.p2p = p2p_args(h);
   return a;
 }
 
@@ -313,37 +356,55 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
 void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, bool record_first) {
   IterArgs a = make_args(h, parity, mode);
   int e = 0;
-  auto mark = [&]() {
+  std::vector<int> side;
+  auto mark = [&](int s) {  // after every launch: event + stream/link side for profiling
+    CK(cudaGetLastError());
     if (ev) CK(cudaEventRecordWithFlags(ev[e], h->stream, cudaEventRecordExternal));
     ++e;
+    side.push_back(s);
   };
-  if (record_first) mark();
-  else ++e;
+  if (record_first) {
+    if (ev) CK(cudaEventRecordWithFlags(ev[0], h->stream, cudaEventRecordExternal));
+  }
+  ++e;
   const int nb = h->nb();
-  k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
-  CK(cudaGetLastError());
-  mark();
+  if (h->p2p) {
+    k_p2p_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
+    mark(1);
+    k_p2p_wait<2, 1><<<1, 32, 0, h->stream>>>(a);
+    mark(1);
+  } else {
+    k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
+    mark(1);
+  }
   for (int b = 0; b < nb; ++b) {
     const BlockArgs bk = block_args(h, b);
     k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
-    CK(cudaGetLastError());
-    mark();
+    mark(1);
     if (b + 1 < nb)
       k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+    else if (h->p2p)
+      k_link_pass<LP_P2P><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else if (!h->sharded)
       k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else
       k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
-    CK(cudaGetLastError());
-    mark();
+    mark(2);
   }
-  if (h->sharded) {
+  if (h->p2p) {
+    k_p2p_wait<0, 0><<<1, 32, 0, h->stream>>>(a);
+    mark(2);
+    k_p2p_epilogue<<<h->grid3, kThreads, 0, h->stream>>>(a);
+    mark(2);
+    k_p2p_finalize<<<1, 32, 0, h->stream>>>(a);
+    mark(2);
+  } else if (h->sharded) {
     NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum, h->comm,
                  h->stream));
     k_link_epilogue<<<h->grid3, kThreads, 0, h->stream>>>(a);
-    CK(cudaGetLastError());
-    mark();
+    mark(2);
   }
+  h->launch_side = side;
 }
 
 cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
@@ -383,8 +444,65 @@ Ctrl read_ctrl(numpmp_gpu* h) {
   return h->ctrl_host[0];
 }
 
+// ------------------------------------------ peer-memory collectives (aux)
+// Outside the iteration loop (pmp_p2p.cuh): every call is collective over
+// the ranks, which run the same sequence.  They use v as the result buffer,
+// so v is marked stale afterwards (rebuilt by k_p2p_refresh_v).
+void p2p_barrier(numpmp_gpu* h, int which) {
+  const P2PArgs p = p2p_args(h);
+  k_p2p_aux_signal<<<1, 32, 0, h->stream>>>(p, which);
+  CK(cudaGetLastError());
+  k_p2p_aux_wait<<<1, 32, 0, h->stream>>>(p, which);
+  CK(cudaGetLastError());
+}
+void p2p_mark_v_stale(numpmp_gpu* h) {
+  static const int one = 1;
+  CK(cudaMemcpyAsync(&h->ctrl->rho_changed, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+// dst[0:m) = sum over ranks of src[0:m) (rank order); src may alias dst.
+void p2p_allreduce(numpmp_gpu* h, const double* src, double* dst) {
+  const P2PArgs p = p2p_args(h);
+  k_p2p_push_partials<<<grid_for(h->m), 256, 0, h->stream>>>(p, src, h->m);
+  CK(cudaGetLastError());
+  p2p_barrier(h, 0);
+  k_p2p_reduce_bcast<<<grid_for(std::max<int64_t>(1, h->l1 - h->l0)), 256, 0, h->stream>>>(p);
+  CK(cudaGetLastError());
+  p2p_barrier(h, 1);
+  CK(cudaMemcpyAsync(dst, h->v, 8 * static_cast<size_t>(h->m), cudaMemcpyDeviceToDevice, h->stream));
+  p2p_barrier(h, 3);
+  p2p_mark_v_stale(h);
+}
+// vec[0:m): every rank receives the owners' values of their links.
+void p2p_allgather_owned(numpmp_gpu* h, double* vec) {
+  const P2PArgs p = p2p_args(h);
+  k_p2p_push_owned<<<grid_for(std::max<int64_t>(1, h->l1 - h->l0)), 256, 0, h->stream>>>(p, vec);
+  CK(cudaGetLastError());
+  p2p_barrier(h, 0);
+  CK(cudaMemcpyAsync(vec, static_cast<char*>(h->xregion) + xr_slots_off(h), 8 * static_cast<size_t>(h->m),
+                     cudaMemcpyDeviceToDevice, h->stream));
+  p2p_barrier(h, 3);
+}
+// d[0:k) (device, k <= 8) = sum over ranks, rank order.
+void p2p_allreduce_scalars(numpmp_gpu* h, double* d, int k) {
+  const P2PArgs p = p2p_args(h);
+  k_p2p_push_scalars<<<1, 32, 0, h->stream>>>(p, d, k);
+  CK(cudaGetLastError());
+  p2p_barrier(h, 1);
+  k_p2p_sum_scalars<<<1, 32, 0, h->stream>>>(p, d, k);
+  CK(cudaGetLastError());
+  p2p_barrier(h, 3);
+}
+// After a run / step the link state (B, zs, price, Q, both iterates) is
+// current only on the owners: gather it on every rank.
+void p2p_sync_link_state(numpmp_gpu* h) {
+  for (int i = 0; i < 2; ++i)
+    for (double* vec : {h->B[i], h->zs[i], h->pr[i], h->Q[i]}) p2p_allgather_owned(h, vec);
+  p2p_mark_v_stale(h);
+}
+
 // Per-link sums of src over this device's columns, block by block in the
-// same order as the link pass (+ NCCL sum when sharded).
+// same order as the link pass (+ the sum over ranks when sharded).
 void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
   IterArgs a = make_args(h, h->cur, MODE_AUX);
   for (int b = 0; b < h->nb(); ++b) {
@@ -394,7 +512,9 @@ void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
       k_link_pass<LP_ROWSUM><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, out);
     CK(cudaGetLastError());
   }
-  if (h->sharded)
+  if (h->p2p)
+    p2p_allreduce(h, out, out);
+  else if (h->sharded)
     NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm, h->stream));
 }
 
@@ -726,6 +846,29 @@ void do_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rh
   reset_ctrl(h, rho > 0.0 ? rho : h->cfg.rho0, 0);
 }
 
+void p2p_wire(numpmp_gpu* h, const std::vector<void*>& bases) {
+  const size_t W = static_cast<size_t>(h->world);
+  std::vector<void*> t(4 * W);
+  for (size_t q = 0; q < W; ++q) {
+    char* b = static_cast<char*>(bases[q]);
+    t[q] = b + xr_slots_off(h);
+    t[W + q] = b;
+    t[2 * W + q] = b + xr_xs_off(h);
+    t[3 * W + q] = b + xr_flags_off(h);
+  }
+  CK(cudaMemcpyAsync(h->peer_tables, t.data(), sizeof(void*) * t.size(), cudaMemcpyHostToDevice,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->p2p = true;
+  for (int i = 0; i < 2; ++i) {  // captured graphs hold the old launch list
+    if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
+    h->graph[i] = nullptr;
+    for (int set = 0; set < 2; ++set) {
+      if (h->prof_graph[i][set]) cudaGraphExecDestroy(h->prof_graph[i][set]);
+      h->prof_graph[i][set] = nullptr;
+    }
+  }
+}
 }  // namespace
 
 // ------------------------------------------------------------------ C-ABI
@@ -746,9 +889,10 @@ int numpmp_gpu_nccl_unique_id(void* out128) {
   return NUMPMP_OK;
 }
 
+// exchange: 0 single device, 1 NCCL all-reduce, 2 peer memory (pmp_p2p.cuh)
 static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, int device,
                        int rank, int world, const void* nccl_id, int64_t stream_begin,
-                       int64_t n_total, numpmp_gpu** out) {
+                       int64_t n_total, numpmp_gpu** out, int exchange = -1) {
   if (!out) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   if (!cfg) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "config is null");
@@ -765,7 +909,17 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
     h->nnz = pv->nnz;
     h->n_total = pv->n;
     h->nnz_total = pv->nnz;
-    if (world >= 1 && nccl_id != nullptr) {
+    if (exchange < 0) exchange = (world >= 1 && nccl_id != nullptr) ? 1 : 0;
+    if (exchange == 2) {
+      if (world < 1 || world > kMaxRanks)
+        throw GpuError{NUMPMP_INVALID_ARGUMENT, "peer-memory exchange supports 1..8 ranks"};
+      h->sharded = true;
+      h->rank = rank;
+      h->world = world;
+      h->stream_begin = stream_begin;
+      h->n_total = n_total;
+      CK(cudaSetDevice(device));
+    } else if (exchange == 1) {
       // Sharded handle (also with world == 1: the same kernels and the
       // same all-reduce, over a one-rank communicator).
       h->sharded = true;
@@ -779,7 +933,24 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
       NK(CommInitRank(&h->comm, world, id, rank));
     }
     create_common(h, pv);
-    if (h->sharded) {
+    if (exchange == 2) {
+      // Exchange region (IPC-exportable, so plain cudaMalloc), v inside it.
+      h->mo = (h->m + world - 1) / world;
+      h->l0 = std::min<int64_t>(h->m, static_cast<int64_t>(rank) * h->mo);
+      h->l1 = std::min<int64_t>(h->m, h->l0 + h->mo);
+      h->xregion_bytes = xr_flags_off(h) + 4 * sizeof(unsigned long long);
+      CK(cudaMalloc(&h->xregion, h->xregion_bytes));
+      CK(cudaMemsetAsync(h->xregion, 0, h->xregion_bytes, h->stream));
+      cudaFreeAsync(h->v, h->stream);
+      h->v = static_cast<double*>(h->xregion);
+      int64_t* b = &h->dev_bytes;
+      h->done_cnt = dalloc<unsigned long long>(4, b, h->stream);
+      CK(cudaMemsetAsync(h->done_cnt, 0, 4 * sizeof(unsigned long long), h->stream));
+      h->ep_part = dalloc<double>(4 * static_cast<size_t>(h->grid3), b, h->stream);
+      h->k1_scalars = dalloc<double>(2, b, h->stream);
+      h->peer_tables = dalloc<void*>(4 * static_cast<size_t>(world), b, h->stream);
+      CK(cudaStreamSynchronize(h->stream));
+    } else if (h->sharded) {
       // Global link degrees and nnz: sums of the shards' local counts.
       NK(AllReduce(h->deg, h->deg, static_cast<size_t>(h->m), ncclInt32, ncclSum, h->comm,
                    h->stream));
@@ -835,6 +1006,97 @@ int numpmp_gpu_create_sharded(const numpmp_problem_view* shard, const numpmp_con
       return set_err((h), NUMPMP_CUDA_ERROR, "host allocation failed"); \
     }                                                                   \
   } while (0)
+
+int numpmp_gpu_create_p2p(const numpmp_problem_view* shard, const numpmp_config* config,
+                          int device, int rank, int world, int64_t stream_begin, int64_t n_total,
+                          numpmp_gpu** out) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "bad rank/world");
+  return create_impl(shard, config, device, rank, world, nullptr, stream_begin, n_total, out, 2);
+}
+
+int numpmp_gpu_p2p_export(numpmp_gpu* h, void* out64) {
+  GUARD(h, {
+    if (!h->xregion) throw GpuError{NUMPMP_INVALID_ARGUMENT, "not a peer-memory handle"};
+    if (!out64) throw GpuError{NUMPMP_INVALID_ARGUMENT, "out is null"};
+    cudaIpcMemHandle_t hd;
+    CK(cudaIpcGetMemHandle(&hd, h->xregion));
+    static_assert(sizeof(hd) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(out64, &hd, sizeof(hd));
+  });
+}
+
+
+int numpmp_gpu_p2p_connect(numpmp_gpu* h, const void* handles) {
+  GUARD(h, {
+    if (!h->xregion || h->p2p)
+      throw GpuError{NUMPMP_INVALID_ARGUMENT, "not an unconnected peer-memory handle"};
+    if (!handles) throw GpuError{NUMPMP_INVALID_ARGUMENT, "handles is null"};
+    CK(cudaSetDevice(h->device));
+    std::vector<void*> bases(static_cast<size_t>(h->world));
+    for (int q = 0; q < h->world; ++q) {
+      if (q == h->rank) {
+        bases[static_cast<size_t>(q)] = h->xregion;
+        continue;
+      }
+      cudaIpcMemHandle_t hd;
+      std::memcpy(&hd, static_cast<const char*>(handles) + 64 * q, sizeof(hd));
+      void* base = nullptr;
+      CK(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+      h->peer_bases.push_back(base);
+      bases[static_cast<size_t>(q)] = base;
+    }
+    p2p_wire(h, bases);
+  });
+}
+
+int numpmp_gpu_p2p_connect_local(numpmp_gpu** hs, int world) {
+  if (!hs || world < 1) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "bad handle list");
+  std::vector<void*> bases(static_cast<size_t>(world));
+  for (int q = 0; q < world; ++q) {
+    if (!hs[q] || !hs[q]->xregion || hs[q]->p2p || hs[q]->world != world || hs[q]->rank != q)
+      return set_err(hs[q], NUMPMP_INVALID_ARGUMENT, "not an unconnected peer-memory handle of this world");
+    bases[static_cast<size_t>(q)] = hs[q]->xregion;
+  }
+  for (int q = 0; q < world; ++q) {
+    numpmp_gpu* h = hs[q];
+    try {
+      CK(cudaSetDevice(h->device));
+      for (int r = 0; r < world; ++r)
+        if (hs[r]->device != h->device) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(hs[r]->device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+          cudaGetLastError();
+        }
+      p2p_wire(h, bases);
+    } catch (const GpuError& e) {
+      return set_err(h, e.code, e.msg);
+    }
+  }
+  return NUMPMP_OK;
+}
+
+int numpmp_gpu_p2p_start(numpmp_gpu* h) {
+  GUARD(h, {
+    if (!h->p2p) throw GpuError{NUMPMP_INVALID_ARGUMENT, "peer-memory handle is not connected"};
+    CK(cudaSetDevice(h->device));
+    // Global link degrees and nnz: sums of the shards' local counts
+    // (exact in fp64).
+    k_int_to_double<<<grid_for(h->m), 256, 0, h->stream>>>(h->deg, h->m, h->scratch_m);
+    CK(cudaGetLastError());
+    p2p_allreduce(h, h->scratch_m, h->scratch_m);
+    k_double_to_int<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->m, h->deg);
+    CK(cudaGetLastError());
+    const double nnz_local = static_cast<double>(h->nnz);
+    CK(cudaMemcpyAsync(h->scalars, &nnz_local, 8, cudaMemcpyHostToDevice, h->stream));
+    p2p_allreduce_scalars(h, h->scalars, 1);
+    double nnz_global = 0.0;
+    CK(cudaMemcpyAsync(&nnz_global, h->scalars, 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->nnz_total = static_cast<int64_t>(nnz_global);
+    do_set_cold(h);
+  });
+}
 
 int numpmp_gpu_set_cold(numpmp_gpu* h) { GUARD(h, do_set_cold(h)); }
 
@@ -978,6 +1240,7 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
 int numpmp_gpu_step(numpmp_gpu* h, double* r_norm, double* s_norm) {
   GUARD(h, {
     enqueue_iteration(h, h->cur, MODE_STEP, nullptr, false);
+    if (h->p2p) p2p_sync_link_state(h);
     const Ctrl c = read_ctrl(h);
     h->cur ^= 1;
     h->iters_since_upload += 1;
@@ -1017,6 +1280,7 @@ void run_loop(numpmp_gpu* h) {
     c.status = ST_RUNNING;
     c.ticket = 0;
     c.ticket2 = 0;
+    c.ticket3 = 0;
     std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
     CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -1039,9 +1303,7 @@ void run_loop(numpmp_gpu* h) {
         float t = 0.f;
         const size_t e0 = static_cast<size_t>(set) * set_size + static_cast<size_t>(i * lpi + l);
         CK(cudaEventElapsedTime(&t, h->prof_ev[e0], h->prof_ev[e0 + 1]));
-        // launch 0 refreshes v (stream side), then stream pass / link
-        // pass alternate; the sharded epilogue (last launch) is link side.
-        if (l == 0 || ((l & 1) == 1 && l < 2 * h->nb()))
+        if (h->launch_side[static_cast<size_t>(l)] == 1)
           h->prof_ms_k1 += t;
         else
           h->prof_ms_k2 += t;
@@ -1081,6 +1343,7 @@ void run_loop(numpmp_gpu* h) {
     h->last_run_ms = ms;
   }
   pt.mark("run: iteration loop");
+  if (h->p2p) p2p_sync_link_state(h);
   h->run_iters = c.run_k;
   h->iters_since_upload += c.run_k;
   h->cur = static_cast<int>((start + c.run_k) & 1);
@@ -1104,7 +1367,9 @@ void post_process(numpmp_gpu* h, double* x, double* s, double* lambda, double* l
   CK(cudaGetLastError());
   k_sum_parts<<<1, kThreads, 0, h->stream>>>(h->k1_part, gpost, h->scalars);
   CK(cudaGetLastError());
-  if (h->sharded)
+  if (h->p2p)
+    p2p_allreduce_scalars(h, h->scalars, 2);
+  else if (h->sharded)
     NK(AllReduce(h->scalars, h->scalars, 2, ncclDouble, ncclSum, h->comm, h->stream));
   global_row_sums(h, h->scratch_n, h->scratch_m);  // load = R x (clamped x)
   k_post_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->cap, h->pr[cu], h->m,
@@ -1267,8 +1532,14 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   PhaseTimer pt;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* base : h->peer_bases) cudaIpcCloseMemHandle(base);
+  if (h->xregion) {
+    cudaFree(h->xregion);
+    h->v = nullptr;  // lived in the exchange region
+  }
   std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
+                             h->done_cnt, h->ep_part, h->k1_scalars, h->peer_tables,
                              h->Lbuf,    h->Lacc,    h->k1_part,   h->k2_part,    h->scratch_m,
                              h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
   for (int i = 0; i < 2; ++i) {

@@ -1,15 +1,23 @@
 """Multi-GPU stream sharding: one process per GPU.
 
 Streams (columns of R) are split into contiguous ranges balanced by
-nonzeros; every rank holds its streams' CSC, a local CSR over all m links,
-and a replicated copy of the link state.  Each iteration the ranks run the
-stream pass locally, sum their partial link loads R_g x_g (plus two scalar
-partials) with one NCCL all-reduce over NVLink inside the device graph, and
-then run the identical replicated link update, so every rank takes the same
-termination and rho decisions without further communication.
+nonzeros; every rank holds its streams' CSC and a local CSR over all m
+links.  Two exchanges are available for the per-iteration sum of the
+partial link loads R_g x_g:
 
-torch.distributed is only plumbing here: it broadcasts the 128-byte NCCL
-unique id that the engine's own communicator is built from.
+* ``exchange="p2p"`` (default): the fused peer-memory exchange of
+  csrc/pmp_p2p.cuh.  Links are owned in contiguous ranges; the link pass
+  stores each row's partial load straight into the owner's HBM over NVLink
+  (overlapped with the remaining gathers), the owner runs the link epilogue
+  for its links only and stores v into every rank's HBM, and all ranks sum
+  the same per-rank residual partials in rank order, so they take the same
+  termination and rho decisions.  No NCCL kernel sits in the loop.
+* ``exchange="nccl"``: replicated link state, one NCCL all-reduce of the m
+  partial loads (+2 scalars) inside the device graph, replicated epilogue.
+  Kept as the library baseline the fused path is measured against.
+
+torch.distributed is only plumbing: it moves the 128-byte NCCL unique id or
+the 64-byte CUDA IPC handles of the exchange regions between the ranks.
 """
 from __future__ import annotations
 
@@ -55,15 +63,63 @@ def nccl_unique_id() -> bytes:
     return bytes(buf.raw)
 
 
-class ShardedPmpSolver:
-    """PmpSolver over this rank's stream shard; link state replicated."""
+def link_owners(m: int, world: int) -> np.ndarray:
+    """Owner ranges of the peer-memory exchange: rank q owns links
+    [b[q], b[q+1]), mo = ceil(m / world) per rank (pmp_solver.cu create_impl)."""
+    mo = -(-m // world)
+    return np.minimum(np.arange(world + 1, dtype=np.int64) * mo, m)
 
-    def __init__(self, problem: Problem, config: SolverConfig, rank: int, world: int, nccl_id: bytes,
-                 device: int = 0):
+
+def p2p_create(problem: Problem, config: SolverConfig, rank: int, world: int, device: int = 0):
+    """Unconnected peer-memory handle of this rank's shard: (handle, local, stream_begin)."""
+    local, j0 = local_shard(problem, rank, world)
+    L = _lib.lib()
+    h = C.c_void_p()
+    view = local.view()
+    rc = L.numpmp_gpu_create_p2p(C.byref(view), C.byref(config._c()), device, rank, world, j0, problem.n,
+                                 C.byref(h))
+    if rc:
+        raise_for(rc, L.numpmp_gpu_last_error(None).decode())
+    return h, local, j0
+
+
+def p2p_export(h) -> bytes:
+    buf = (C.c_char * 64)()
+    L = _lib.lib()
+    rc = L.numpmp_gpu_p2p_export(h, buf)
+    if rc:
+        raise_for(rc, L.numpmp_gpu_last_error(h).decode())
+    return bytes(buf.raw)
+
+
+class ShardedPmpSolver:
+    """PmpSolver over this rank's stream shard (see the module docstring).
+
+    exchange="p2p" needs ``ipc_allgather``: a callable taking this rank's
+    64-byte handle and returning the rank-ordered list of all ranks' handles
+    (e.g. torch.distributed.all_gather_object).  Construction is collective.
+    """
+
+    def __init__(self, problem: Problem, config: SolverConfig, rank: int, world: int, nccl_id: bytes = None,
+                 device: int = 0, exchange: str = "nccl", ipc_allgather=None, handle=None):
         self.full = problem
-        self.local, self.stream_begin = local_shard(problem, rank, world)
         self._cfg = config
+        self.exchange = exchange
         L = _lib.lib()
+        if handle is not None:  # an already connected peer-memory handle (in-process ranks)
+            self._h = handle
+            self.local, self.stream_begin = local_shard(problem, rank, world)
+            return
+        if exchange == "p2p":
+            h, self.local, self.stream_begin = p2p_create(problem, config, rank, world, device)
+            self._h = h
+            handles = ipc_allgather(p2p_export(h))
+            blob = C.create_string_buffer(b"".join(handles), 64 * world)
+            for rc in (L.numpmp_gpu_p2p_connect(h, blob), L.numpmp_gpu_p2p_start(h)):
+                if rc:
+                    raise_for(rc, L.numpmp_gpu_last_error(h).decode())
+            return
+        self.local, self.stream_begin = local_shard(problem, rank, world)
         h = C.c_void_p()
         view = self.local.view()
         idbuf = C.create_string_buffer(nccl_id, 128)
@@ -75,6 +131,12 @@ class ShardedPmpSolver:
 
     def handle(self):
         return self._h
+
+    def _start(self):
+        L = _lib.lib()
+        rc = L.numpmp_gpu_p2p_start(self._h)
+        if rc:
+            raise_for(rc, L.numpmp_gpu_last_error(self._h).decode())
 
     def solve(self) -> Solution:
         """Cold solve; x is this rank's shard, link vectors are global."""
@@ -104,3 +166,44 @@ class ShardedPmpSolver:
             self.close()
         except Exception:
             pass
+
+
+def p2p_local_group(problem: Problem, config: SolverConfig, world: int, device: int = 0):
+    """`world` peer-memory ranks of one problem inside this process (one GPU,
+    or several with peer access), wired and started.  Every collective call
+    on them (solve, set_warm, step) must then be made from one thread per
+    rank, e.g. with run_ranks()."""
+    L = _lib.lib()
+    made = [p2p_create(problem, config, r, world, device) for r in range(world)]
+    arr = (C.c_void_p * world)(*[m[0] for m in made])
+    rc = L.numpmp_gpu_p2p_connect_local(arr, world)
+    if rc:
+        raise_for(rc, L.numpmp_gpu_last_error(None).decode())
+    solvers = [ShardedPmpSolver(problem, config, r, world, exchange="p2p", handle=made[r][0]) for r in range(world)]
+    run_ranks([lambda s=s: s._start() for s in solvers])
+    return solvers
+
+
+def run_ranks(fns):
+    """Run one callable per rank concurrently (threads; the C calls release
+    the GIL) and return their results in rank order; re-raises the first error."""
+    import threading
+
+    out = [None] * len(fns)
+    err = [None] * len(fns)
+
+    def go(i):
+        try:
+            out[i] = fns[i]()
+        except BaseException as e:  # noqa: BLE001
+            err[i] = e
+
+    ts = [threading.Thread(target=go, args=(i,)) for i in range(len(fns))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out

@@ -290,6 +290,60 @@ def test_sharded_path_one_rank_matches_oracle(blocks, restatement, oracle_mod, m
     assert abs(sol.objective - ref.objective) <= RTOL * abs(ref.objective)
 
 
+@pytest.mark.parametrize("world,blocks", [(1, 1), (2, 1), (3, 2), (4, 1)])
+def test_p2p_exchange_ranks_match_oracle(world, blocks, restatement, oracle_mod, monkeypatch):
+    # The fused peer-memory exchange (csrc/pmp_p2p.cuh) with `world` ranks in
+    # this process on one GPU, each driven by its own host thread exactly as
+    # one process per GPU would drive it: link-pass stores into the owners'
+    # slots, system-scope barriers, owner epilogue + v broadcast, rank-order
+    # sums.  The assembled solution must match the single-problem oracle at
+    # equal iteration counts (mixed utilities, several rho changes).
+    from paper_2509_10722_b200.shard import link_owners, p2p_local_group, run_ranks
+
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", str(blocks))
+    p = _gen(2000, 4000, 6.0, 2, True, 11)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    ranks = p2p_local_group(p, cfg, world)
+    try:
+        sols = run_ranks([s.solve for s in ranks])
+    finally:
+        for s in ranks:
+            s.close()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    x = np.concatenate([s.x for s in sols])
+    for s in sols:
+        assert s.iterations == ref.iterations
+        # every rank holds the same gathered link vectors and scalars
+        np.testing.assert_array_equal(s.lambda_raw, sols[0].lambda_raw)
+        assert s.r_norm == sols[0].r_norm and s.s_norm == sols[0].s_norm
+    for got, want in [(x, ref.x), (sols[0].lambda_raw, ref.lambda_raw), (sols[0].s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
+    assert abs(sols[0].objective - ref.objective) <= RTOL * abs(ref.objective)
+    assert [r.iter for r in sols[0].trace] == [r.iter for r in ref.trace]
+    assert link_owners(p.m, world)[-1] == p.m
+
+
+def test_p2p_exchange_is_deterministic(monkeypatch):
+    # rank-order sums: identical bytes on a rerun, whatever the arrival order
+    from paper_2509_10722_b200.shard import p2p_local_group, run_ranks
+
+    p = _gen(1500, 3000, 5.0, 2, True, 5)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    outs = []
+    for _ in range(2):
+        ranks = p2p_local_group(p, cfg, 3)
+        try:
+            outs.append(run_ranks([s.solve for s in ranks]))
+        finally:
+            for s in ranks:
+                s.close()
+    for a, b in zip(*outs):
+        assert a.iterations == b.iterations
+        np.testing.assert_array_equal(a.x, b.x)
+        np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
+
+
 @pytest.mark.parametrize("K", [1, 10, 100])
 def test_step_state_matches_oracle(K, restatement, oracle_mod):
     # state-level parity of step() on config A
