@@ -320,7 +320,7 @@ def test_p2p_exchange_ranks_match_oracle(world, blocks, restatement, oracle_mod,
         ok, err = close(got, want)
         assert ok, err
     assert abs(sols[0].objective - ref.objective) <= RTOL * abs(ref.objective)
-    assert [r.iter for r in sols[0].trace] == [r.iter for r in ref.trace]
+    assert [r.iter for r in sols[0].trace] == [int(i) for i in ref.trace[:, 0]]
     assert link_owners(p.m, world)[-1] == p.m
 
 
@@ -566,3 +566,61 @@ def test_config_c_full_solve_properties():
     assert np.max(np.abs(viol)) <= 10.0 * eps_tol
     assert np.min(sol.x) >= -1e-4
     assert np.min(sol.lambda_) >= 0.0
+
+
+def _ipc_rank(rank, world, port, q):
+    # one process per rank, all on cuda:0 (the box has one GPU): the real
+    # CUDA IPC path of the exchange (export -> all_gather -> open), gloo for
+    # the 64-byte handles
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2509_10722_b200 as pmp_
+    from paper_2509_10722_b200.shard import ShardedPmpSolver
+
+    p = _gen(1200, 2500, 5.0, 2, True, 3)
+    cfg = pmp_.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+
+    def ipc_allgather(mine):
+        out = [None] * world
+        dist.all_gather_object(out, mine)
+        return out
+
+    s = ShardedPmpSolver(p, cfg, rank, world, device=0, exchange="p2p", ipc_allgather=ipc_allgather)
+    sol = s.solve()
+    s.close()
+    q.put((rank, s.stream_begin, sol.x, sol.lambda_raw, sol.iterations))
+    dist.destroy_process_group()
+
+
+def test_p2p_exchange_over_cuda_ipc_processes(restatement, oracle_mod):
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = _gen(1200, 2500, 5.0, 2, True, 3)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    x = np.concatenate([r[2] for r in sorted(res, key=lambda t: t[1])])
+    assert all(r[4] == ref.iterations for r in res)
+    for got, want in [(x, ref.x), (res[0][3], ref.lambda_raw)]:
+        ok, err = close(got, want)
+        assert ok, err

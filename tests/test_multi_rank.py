@@ -141,3 +141,133 @@ def test_two_rank_sharded_iteration_matches_oracle(restatement, oracle_mod):
         assert abs(rs[k][1] - s) <= 1e-7 * max(s, 1e-300)
     np.testing.assert_allclose(xfull, x, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(price, st["price"], rtol=1e-9, atol=1e-12)
+
+
+# ------------------------------------------------ peer-memory (owner) exchange
+def _owner_iterations(rank, world, p, cfg, K):
+    """K iterations of the owner-computes decomposition of csrc/pmp_p2p.cuh:
+    partial loads go to the owner of each link (here an all_gather stands in
+    for the NVLink stores into the owner's slots), the owner sums the ranks'
+    partials in rank order and runs the epilogue for its links only, v of the
+    owned links is broadcast (all_gather), the per-rank residual partials are
+    summed in rank order on every rank, and after a rho change v is rebuilt
+    by the owners from their own B and price."""
+    from paper_2509_10722_b200.shard import link_owners, local_shard
+
+    q, s0 = local_shard(p, rank, world)
+    m = p.m
+    own = link_owners(m, world)
+    l0, l1 = int(own[rank]), int(own[rank + 1])
+    mo = int(own[1] - own[0])
+    tau = np.diff(q.stream_offsets)
+    seg = np.repeat(np.arange(q.n), tau)
+    A = np.zeros(q.n)
+    B = np.zeros(m)      # current only on [l0, l1) after the first iteration
+    zs = np.zeros(m)
+    price = np.zeros(m)
+    Q = np.zeros(m)
+    rho = cfg["rho0"]
+    alpha, mu, gamma, interval = cfg["alpha"], cfg["mu"], cfg["gamma"], cfg["interval"]
+    d_local = np.bincount(q.route_links, minlength=m).astype(np.float64)
+    t = torch.from_numpy(d_local)
+    dist.all_reduce(t)
+    deg = t.numpy()
+
+    def allgather_owned(vec_owned):
+        pad = np.zeros(mo)
+        pad[: l1 - l0] = vec_owned
+        parts = [torch.zeros(mo, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(pad))
+        return np.concatenate([x.numpy() for x in parts])[:m]
+
+    v = B + price / rho
+    rs = []
+    for k in range(1, K + 1):
+        zeta = tau * A - np.bincount(seg, weights=v[q.route_links], minlength=q.n)
+        x = _prox(zeta, q.weights, rho, tau, q.kinds)
+        An = alpha * x + (1.0 - alpha) * A
+        tda2 = np.sum(tau * (An - A) ** 2)
+        A = An
+        L_local = np.bincount(q.route_links, weights=x[seg], minlength=m)
+        parts = [torch.zeros(m, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(L_local))
+        L = np.zeros(l1 - l0)
+        for r in range(world):  # rank order
+            L = L + parts[r].numpy()[l0:l1]
+        sl = slice(l0, l1)
+        ps = np.maximum(zs[sl] - price[sl] / rho, -p.capacities[sl])
+        pbar = (L + ps) / (deg[sl] + 1.0)
+        Bn = alpha * pbar + (1.0 - alpha) * B[sl]
+        zsn = alpha * (ps - pbar) + (1.0 - alpha) * zs[sl]
+        Qn = alpha * L + (1.0 - alpha) * Q[sl]
+        row = np.array([tda2, np.sum((deg[sl] + 1.0) * pbar * pbar), np.sum((Bn - B[sl]) * (Qn - Q[sl])),
+                        np.sum(deg[sl] * (Bn - B[sl]) ** 2), np.sum((zsn - zs[sl]) ** 2)])
+        price[sl] = price[sl] + rho * (alpha * pbar)
+        B[sl], zs[sl], Q[sl] = Bn, zsn, Qn
+        v = allgather_owned(B[sl] + price[sl] / rho)
+        rows = [torch.zeros(5, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(rows, torch.from_numpy(row))
+        tot = np.zeros(5)
+        for r in range(world):
+            tot = tot + rows[r].numpy()
+        r_n = np.sqrt(tot[1])
+        s_n = np.sqrt(max(rho * rho * (tot[0] - 2.0 * tot[2] + tot[3] + tot[4]), 0.0))
+        rs.append((r_n, s_n))
+        if k % interval == 0:  # update_rho, identical on every rank
+            new = rho * gamma if r_n > mu * s_n else (rho / gamma if s_n > mu * r_n else rho)
+            if new != rho:
+                rho = new
+                v = allgather_owned(B[sl] + price[sl] / rho)  # k_p2p_refresh_v
+    return s0, x, allgather_owned(price[l0:l1]), rs, rho
+
+
+def _owner_worker(rank, world, port, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2509_10722_b200 as pmp
+
+    p = pmp.gen_uncongested(pmp.GenSpec(m=301, n=900, avg_links_per_stream=5.0, kind=pmp.GenKind.Mixed,
+                                        weights=pmp.WeightDist.uniform(0.5, 1.5), seed=29))
+    cfg = dict(rho0=1.0, alpha=1.6, mu=2.0, gamma=1.1, interval=5)
+    s0, x, price, rs, rho = _owner_iterations(rank, world, p, cfg, 40)
+    xs = [None] * world
+    dist.all_gather_object(xs, (s0, x))
+    if rank == 0:
+        xfull = np.concatenate([xi for _, xi in sorted(xs, key=lambda a: a[0])])
+        result_q.put((xfull, price, rs, rho))
+    dist.destroy_process_group()
+
+
+def test_three_rank_owner_exchange_matches_oracle(restatement, oracle_mod):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_owner_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    xfull, price, rs, rho = q.get(timeout=300)
+    assert rho != 1.0  # the run crossed rho changes (the owners' v refresh)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+
+    import paper_2509_10722_b200 as pmp
+
+    p = pmp.gen_uncongested(pmp.GenSpec(m=301, n=900, avg_links_per_stream=5.0, kind=pmp.GenKind.Mixed,
+                                        weights=pmp.WeightDist.uniform(0.5, 1.5), seed=29))
+    a = oracle_mod.arrays_from(p)
+    cfg = oracle_mod.Config(rho0=1.0, alpha=1.6, rho_update_interval=5)
+    st = restatement.cold_state(a, cfg)
+    for k in range(40):
+        r, s, x = restatement.step(a, cfg, st)
+        assert abs(rs[k][0] - r) <= 1e-9 * max(r, 1e-300)
+        assert abs(rs[k][1] - s) <= 1e-7 * max(s, 1e-300)
+        if (k + 1) % 5 == 0:  # step() has no rho control: update_rho as run() does (solver.hpp:168-174)
+            if r > 2.0 * s:
+                st["rho"] = st["rho"] * 1.1
+            elif s > 2.0 * r:
+                st["rho"] = st["rho"] / 1.1
+    np.testing.assert_allclose(xfull, x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(price, st["price"], rtol=1e-9, atol=1e-12)
