@@ -148,6 +148,26 @@ int numpmp_gpu_set_cold(numpmp_gpu* h);
  * x0 length n, price length m; log streams need x0 > 0 (NUMPMP_DOMAIN_ERROR). */
 int numpmp_gpu_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rho);
 
+/* Warm-start recipes of warm.hpp computed on the device and applied with
+ * warm_start_from (solver.hpp:218-259) without a host round trip.
+ * numpmp_gpu_warm_after_degrade replaces warm_start_after_degrade
+ * (warm.hpp:25-57): the handle holds the degraded problem; cap_before[m] is
+ * the prior problem's capacities, prior_x[n] / prior_lambda_raw[m] /
+ * prior_rho the prior Solution.  numpmp_gpu_warm_after_prune replaces
+ * warm_start_after_prune (warm.hpp:62-94): the handle holds the pruned
+ * problem; x0_proj[n] / price_proj[m] are the prior x and lambda_raw already
+ * projected with PruneMap::project_streams / project_links (gen.hpp:146-178).
+ * The optional outputs return the recipe's WarmStart (x0, price, rho). */
+int numpmp_gpu_warm_after_degrade(numpmp_gpu* h, const double* cap_before, const double* prior_x,
+                                  const double* prior_lambda_raw, double prior_rho, double* x0_out,
+                                  double* price_out, double* rho_out);
+int numpmp_gpu_warm_after_prune(numpmp_gpu* h, const double* x0_proj, const double* price_proj,
+                                double prior_rho, double* x0_out, double* price_out, double* rho_out);
+
+/* Replaces path_prices (transit.hpp:290-302): pi[n] = sum of lambda[m]
+ * along each stream's route, in route order. */
+int numpmp_gpu_path_prices(numpmp_gpu* h, const double* lambda, double* pi);
+
 /* Loads an arbitrary reference SolverState (solver.hpp:51-62): p, z of
  * length J = nnz + m, p_bar and price of length m.  z must decompose as
  * z_t = A_j - B_l over the incidence (every cold, warm and stepped state

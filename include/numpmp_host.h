@@ -8,6 +8,7 @@
  *   numpmp_gen_uncongested  gen.hpp:61-97 + rng.hpp:17-77
  *   numpmp_gen_congested    gen.hpp:103-128
  *   numpmp_degrade          gen.hpp:132-143
+ *   numpmp_fail_and_prune   gen.hpp:146-223
  *   numpmp_validate         model.hpp:76-155 (+ violations_message 203-215)
  *   numpmp_build_layout     model.hpp:159-201
  */
@@ -69,6 +70,12 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
 
 /* In-place capacity degradation with the reference's draw order. */
 int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor, uint64_t seed);
+/* fail_and_prune (gen.hpp:181-223): the pruned instance plus the PruneMap
+ * (gen.hpp:146-178): link_map[m] (new id or -1), stream_map[n] (new id or -1). */
+int numpmp_fail_and_prune(int64_t m, int64_t n, const double* capacities, const double* weights,
+                          const uint8_t* kinds, const int64_t* offsets, const int32_t* routes,
+                          double p_fail, uint64_t seed, numpmp_instance** out, int32_t* link_map,
+                          int64_t* stream_map);
 
 /* Model validation; returns the number of violations and writes the
  * reference's "invalid problem: [...]" message (truncated to msg_cap). */

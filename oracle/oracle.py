@@ -244,6 +244,7 @@ class Reference:
                                       C.POINTER(P), C.POINTER(I64)]
         L.ref_degrade.argtypes = [P, D, D, C.c_uint64, C.POINTER(P)]
         L.ref_fail_and_prune.argtypes = [P, D, C.c_uint64, C.POINTER(P)]
+        L.ref_prune_maps.argtypes = [P, P, P]
         L.ref_build_problem.argtypes = [I64, I64, P, P, P, P, P, C.POINTER(P)]
         L.ref_sizes.argtypes = [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]
         L.ref_free.argtypes = [P]
@@ -339,7 +340,16 @@ class RefProblem:
     def fail_and_prune(self, p_fail, seed) -> "RefProblem":
         h = P()
         self.ref._err(self.ref.L.ref_fail_and_prune(self.h, p_fail, seed, C.byref(h)))
-        return RefProblem(self.ref, h)
+        out = RefProblem(self.ref, h)
+        out.prior_m, out.prior_n = self.m, self.n
+        return out
+
+    def prune_maps(self):
+        """(link_map[prior m], stream_map[prior n]) of a fail_and_prune result."""
+        lm = np.empty(self.prior_m, np.int32)
+        sm = np.empty(self.prior_n, np.int64)
+        self.ref.L.ref_prune_maps(self.h, _p(lm), _p(sm))
+        return lm, sm
 
     def solve(self, cfg: Config, warm=None, final_state=False) -> Result:
         d, i = _cfg_arrays(cfg)

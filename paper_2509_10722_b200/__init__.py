@@ -18,7 +18,9 @@ from .model import (
     TransitSpec,
     WeightDist,
     build_problem,
+    PruneMap,
     degrade,
+    fail_and_prune,
     gen_congested,
     gen_transit,
     gen_uncongested,
@@ -43,7 +45,7 @@ from .solver import (
 __all__ = [
     "DeviceError", "DomainError", "GenError", "SolverError", "ValidationError",
     "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitSpec", "WeightDist",
-    "build_problem", "degrade", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "validate",
+    "build_problem", "degrade", "fail_and_prune", "PruneMap", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "validate",
     "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
     "check_termination", "objective", "recover_duals", "to_string", "update_rho",
 ]

@@ -116,6 +116,9 @@ SIGNATURES = {
     "numpmp_gpu_p2p_connect": (C.c_int, [P, P]),
     "numpmp_gpu_p2p_connect_local": (C.c_int, [C.POINTER(P), C.c_int]),
     "numpmp_gpu_p2p_start": (C.c_int, [P]),
+    "numpmp_gpu_warm_after_degrade": (C.c_int, [P, P, P, P, D, P, P, PD]),
+    "numpmp_gpu_warm_after_prune": (C.c_int, [P, P, P, D, P, P, PD]),
+    "numpmp_gpu_path_prices": (C.c_int, [P, P, P]),
     "numpmp_gpu_set_cold": (C.c_int, [P]),
     "numpmp_gpu_set_warm": (C.c_int, [P, P, P, D]),
     "numpmp_gpu_set_state": (C.c_int, [P, P, P, P, P, D, I64]),
@@ -138,6 +141,7 @@ SIGNATURES = {
     "numpmp_instance_free": (None, [P]),
     "numpmp_gen_transit": (C.c_int, [C.POINTER(TransitSpecC), C.POINTER(P), PI64]),
     "numpmp_degrade": (C.c_int, [I64, P, D, D, C.c_uint64]),
+    "numpmp_fail_and_prune": (C.c_int, [I64, I64, P, P, P, P, P, D, C.c_uint64, C.POINTER(P), P, P]),
     "numpmp_validate": (I64, [I64, I64, P, P, P, P, P, C.c_char_p, I64]),
     "numpmp_build_layout": (C.c_int, [I64, I64, P, P, P, P, P, P]),
     "numpmp_host_last_error": (C.c_char_p, []),

@@ -465,6 +465,66 @@ int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double facto
   return 0;
 }
 
+int numpmp_fail_and_prune(int64_t m, int64_t n, const double* capacities, const double* weights,
+                          const uint8_t* kinds, const int64_t* offsets, const int32_t* routes,
+                          double p_fail, uint64_t seed, numpmp_instance** out, int32_t* link_map,
+                          int64_t* stream_map) {
+  // gen.hpp:181-223: each link fails with probability p_fail (one draw per
+  // link, in order); failed links and every stream crossing one are removed;
+  // survivors are reindexed densely in order.
+  if (!(p_fail >= 0.0 && p_fail < 1.0)) {
+    g_host_err = "fail_and_prune: probability must be in [0, 1)";
+    return 5;
+  }
+  Rng rng(seed);
+  std::vector<char> failed(static_cast<std::size_t>(m), 0);
+  for (auto& f : failed) f = rng.bernoulli(p_fail) ? 1 : 0;
+  auto* inst = new numpmp_instance();
+  std::int32_t next_link = 0;
+  for (int64_t l = 0; l < m; ++l) {
+    if (failed[static_cast<std::size_t>(l)]) {
+      link_map[l] = -1;
+      continue;
+    }
+    link_map[l] = next_link++;
+    inst->capacities.push_back(capacities[l]);
+  }
+  if (next_link == 0) {
+    delete inst;
+    g_host_err = "fail_and_prune: all links failed";
+    return 5;
+  }
+  inst->offsets.push_back(0);
+  int64_t next_stream = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    bool hit = false;
+    for (int64_t t = offsets[j]; t < offsets[j + 1]; ++t)
+      if (failed[static_cast<std::size_t>(routes[t])]) {
+        hit = true;
+        break;
+      }
+    if (hit) {
+      stream_map[j] = -1;
+      continue;
+    }
+    for (int64_t t = offsets[j]; t < offsets[j + 1]; ++t)
+      inst->routes.push_back(link_map[routes[t]]);
+    inst->offsets.push_back(static_cast<int64_t>(inst->routes.size()));
+    inst->weights.push_back(weights[j]);
+    inst->kinds.push_back(kinds[j]);
+    stream_map[j] = next_stream++;
+  }
+  if (next_stream == 0) {
+    delete inst;
+    g_host_err = "fail_and_prune: no stream survived the failures";
+    return 5;
+  }
+  inst->m = next_link;
+  inst->n = next_stream;
+  *out = inst;
+  return 0;
+}
+
 int64_t numpmp_validate(int64_t m, int64_t n, const double* capacities, const double* weights,
                         const uint8_t* kinds, const int64_t* offsets, const int32_t* routes,
                         char* msg, int64_t msg_cap) {

@@ -234,6 +234,87 @@ __global__ void k_sum_parts(const double* __restrict__ part, int count, double* 
 
 __global__ void k_start_clock(Ctrl* c) { c->t0_ns = globaltimer_ns(); }
 
+// ---------------------------------------------- warm-start recipes (warm.hpp)
+// ratio_l = c_after / c_before; price_l = lambda_raw_l / ratio_l (warm.hpp:29-51).
+__global__ void k_degrade_links(const double* __restrict__ cap_after, long long m,
+                                double* __restrict__ ratio, double* __restrict__ price) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double r = cap_after[l] / ratio[l];
+    ratio[l] = r;
+    price[l] = price[l] / r;
+  }
+}
+// x0_j *= min over the route of ratio (std::min, route order); log streams
+// floored at 1e-8 (warm.hpp:42-49).
+__global__ void k_route_min_scale(const int* __restrict__ col_ptr, const int* __restrict__ row_idx,
+                                  long long n, const double* __restrict__ ratio,
+                                  const unsigned char* __restrict__ kind, double* __restrict__ x) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    double cut = 1.0;
+    for (int t = col_ptr[j]; t < col_ptr[j + 1]; ++t) {
+      const double r = ratio[row_idx[t]];
+      cut = (r < cut) ? r : cut;
+    }
+    double v = x[j] * cut;
+    if (kind[j] == NUMPMP_KIND_LOG && !(v > 0.0)) v = 1e-8;
+    x[j] = v;
+  }
+}
+// transit.hpp:290-302 path_prices: pi_j = sum of lambda along the route, in
+// route order.
+__global__ void k_path_prices(const int* __restrict__ col_ptr, const int* __restrict__ row_idx,
+                              long long n, const double* __restrict__ lambda, double* __restrict__ pi) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    double total = 0.0;
+    for (int t = col_ptr[j]; t < col_ptr[j + 1]; ++t) total += lambda[row_idx[t]];
+    pi[j] = total;
+  }
+}
+// warm.hpp:73-82: price_l *= min(1, load_l / c_l); clamped = max(price, 0).
+__global__ void k_prune_prices(const double* __restrict__ load, const double* __restrict__ cap,
+                               long long m, double* __restrict__ price, double* __restrict__ clamped) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double f = load[l] / cap[l];
+    const double p = price[l] * ((f < 1.0) ? f : 1.0);
+    price[l] = p;
+    clamped[l] = (p < 0.0) ? 0.0 : p;
+  }
+}
+// warm.hpp:84-91: log streams re-centred on the path price.
+__global__ void k_recenter_log(const double* __restrict__ pi, const double* __restrict__ w,
+                               const unsigned char* __restrict__ kind, long long n,
+                               double* __restrict__ x) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    if (kind[j] != NUMPMP_KIND_LOG) continue;
+    double v = x[j];
+    if (pi[j] > 1e-10) v = w[j] / pi[j];
+    if (!(v > 0.0)) v = 1e-8;
+    x[j] = v;
+  }
+}
+// Per-link sums in ascending stream order over the column blocks' CSRs (one
+// accumulator per link, the reference's loop order).
+struct BlockCsrs {
+  const int* row_ptr[kMaxBlocks];
+  const int* col_idx[kMaxBlocks];
+  int nblocks;
+};
+__global__ void k_row_sums_seq(BlockCsrs bc, long long m, const double* __restrict__ src,
+                               double* __restrict__ out) {
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;
+       l += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < bc.nblocks; ++b)
+      for (int k = bc.row_ptr[b][l]; k < bc.row_ptr[b][l + 1]; ++k) acc += src[bc.col_idx[b][k]];
+    out[l] = acc;
+  }
+}
+
 __global__ void k_int_to_double(const int* __restrict__ in, long long count, double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x)

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "numpmp_gpu.h"
@@ -818,6 +819,8 @@ void do_set_cold(numpmp_gpu* h) {
   reset_ctrl(h, h->cfg.rho0, 0);
 }
 
+void set_warm_from_device(numpmp_gpu* h, double rho);
+
 // warm_state (solver.hpp:305-314) + warm_start_from (218-259).
 void do_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rho) {
   if (!x0) throw GpuError{NUMPMP_INVALID_ARGUMENT, "warm start: x0 length does not match n"};
@@ -828,22 +831,108 @@ void do_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rh
       throw GpuError{NUMPMP_DOMAIN_ERROR, "warm start: log stream " +
                                               std::to_string(j + h->stream_begin) +
                                               " needs a positive rate"};
-  h->cur = 0;
   const size_t nb = 8 * static_cast<size_t>(h->n), mb = 8 * static_cast<size_t>(h->m);
   upload(h, h->x, x0, nb);
+  if (price)
+    upload(h, h->pr[0], price, mb);
+  else
+    CK(cudaMemsetAsync(h->pr[0], 0, mb, h->stream));
+  set_warm_from_device(h, rho);
+}
+
+// warm_start_from (solver.hpp:218-259) with x0 already in h->x and the
+// prices in h->pr[0] (device): A = x0, load = R x0, B / zs / Q / slack.
+void set_warm_from_device(numpmp_gpu* h, double rho) {
+  h->cur = 0;
+  const size_t nb = 8 * static_cast<size_t>(h->n);
   CK(cudaMemcpyAsync(h->A[0], h->x, nb, cudaMemcpyDeviceToDevice, h->stream));
   global_row_sums(h, h->x, h->scratch_m);  // load = R x0
   k_warm_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->deg, nullptr, h->cap,
                                                        h->m, h->B[0], h->zs[0], h->Q[0], h->ps0,
                                                        h->pbar0);
   CK(cudaGetLastError());
-  if (price)
-    upload(h, h->pr[0], price, mb);
-  else
-    CK(cudaMemsetAsync(h->pr[0], 0, mb, h->stream));
   h->host_p_valid = false;
   h->iters_since_upload = 0;
   reset_ctrl(h, rho > 0.0 ? rho : h->cfg.rho0, 0);
+}
+
+// Per-link sums of src over this device's columns in the reference's order
+// (ascending stream id, one accumulator per link, model.hpp / warm.hpp
+// loops): bit-exact with the host loops on one device.
+void row_sums_sequential(numpmp_gpu* h, const double* src, double* out) {
+  BlockCsrs bc{};
+  bc.nblocks = h->nb();
+  for (int b = 0; b < h->nb(); ++b) {
+    bc.row_ptr[b] = h->blocks[static_cast<size_t>(b)].row_ptr;
+    bc.col_idx[b] = h->blocks[static_cast<size_t>(b)].col_idx;
+  }
+  k_row_sums_seq<<<grid_for(h->m), 256, 0, h->stream>>>(bc, h->m, src, out);
+  CK(cudaGetLastError());
+  if (h->p2p)
+    p2p_allreduce(h, out, out);
+  else if (h->sharded)
+    NK(AllReduce(out, out, static_cast<size_t>(h->m), ncclDouble, ncclSum, h->comm, h->stream));
+}
+
+// warm.hpp:25-57 warm_start_after_degrade on the device: the handle holds
+// the degraded problem; cap_before, prior_x (this handle's streams) and
+// prior_lambda_raw are the prior problem's capacities and solution.
+void do_warm_after_degrade(numpmp_gpu* h, const double* cap_before, const double* prior_x,
+                           const double* prior_lambda_raw, double prior_rho, double* x0_out,
+                           double* price_out, double* rho_out) {
+  if (!cap_before || !prior_x || !prior_lambda_raw)
+    throw GpuError{NUMPMP_INVALID_ARGUMENT, "degrade warm start: null input"};
+  const size_t nb = 8 * static_cast<size_t>(h->n), mb = 8 * static_cast<size_t>(h->m);
+  double* ratio = h->scratch_m2;
+  upload(h, ratio, cap_before, mb);                 // c_before -> ratio = c_after / c_before
+  upload(h, h->pr[0], prior_lambda_raw, mb);
+  upload(h, h->x, prior_x, nb);
+  k_degrade_links<<<grid_for(h->m), 256, 0, h->stream>>>(h->cap, h->m, ratio, h->pr[0]);
+  CK(cudaGetLastError());
+  k_route_min_scale<<<grid_for(h->n), 256, 0, h->stream>>>(h->col_ptr, h->row_idx, h->n, ratio,
+                                                           h->kind, h->x);
+  CK(cudaGetLastError());
+  // worst cut = min over links (exact in any order)
+  size_t temp_bytes = 0;
+  CK(cub::DeviceReduce::Min(nullptr, temp_bytes, ratio, h->scalars, static_cast<int>(h->m), h->stream));
+  void* temp = nullptr;
+  CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
+  CK(cub::DeviceReduce::Min(temp, temp_bytes, ratio, h->scalars, static_cast<int>(h->m), h->stream));
+  double worst = 1.0;
+  CK(cudaMemcpyAsync(&worst, h->scalars, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFreeAsync(temp, h->stream);
+  worst = std::min(1.0, worst);  // warm.hpp:33-41 starts from worst_cut = 1.0
+  const double rho = prior_rho / worst;
+  if (x0_out) download(h, x0_out, h->x, nb);
+  if (price_out) download(h, price_out, h->pr[0], mb);
+  if (rho_out) *rho_out = rho;
+  set_warm_from_device(h, rho);
+}
+
+// warm.hpp:62-94 warm_start_after_prune on the device.  x0 / price are the
+// prior solution already projected onto the survivors (PruneMap::project_*,
+// a host gather by the caller).
+void do_warm_after_prune(numpmp_gpu* h, const double* x0_proj, const double* price_proj,
+                         double prior_rho, double* x0_out, double* price_out, double* rho_out) {
+  if (!x0_proj || !price_proj) throw GpuError{NUMPMP_INVALID_ARGUMENT, "prune warm start: null input"};
+  const size_t nb = 8 * static_cast<size_t>(h->n), mb = 8 * static_cast<size_t>(h->m);
+  upload(h, h->x, x0_proj, nb);
+  upload(h, h->pr[0], price_proj, mb);
+  row_sums_sequential(h, h->x, h->scratch_m);  // load, in the reference's order
+  k_prune_prices<<<grid_for(h->m), 256, 0, h->stream>>>(h->scratch_m, h->cap, h->m, h->pr[0],
+                                                        h->scratch_m2);
+  CK(cudaGetLastError());
+  k_path_prices<<<grid_for(h->n), 256, 0, h->stream>>>(h->col_ptr, h->row_idx, h->n, h->scratch_m2,
+                                                       h->scratch_n);
+  CK(cudaGetLastError());
+  k_recenter_log<<<grid_for(h->n), 256, 0, h->stream>>>(h->scratch_n, h->w, h->kind, h->n, h->x);
+  CK(cudaGetLastError());
+  if (x0_out) download(h, x0_out, h->x, nb);
+  if (price_out) download(h, price_out, h->pr[0], mb);
+  if (rho_out) *rho_out = prior_rho;
+  CK(cudaStreamSynchronize(h->stream));
+  set_warm_from_device(h, prior_rho);
 }
 
 void p2p_wire(numpmp_gpu* h, const std::vector<void*>& bases) {
@@ -1099,6 +1188,30 @@ int numpmp_gpu_p2p_start(numpmp_gpu* h) {
 }
 
 int numpmp_gpu_set_cold(numpmp_gpu* h) { GUARD(h, do_set_cold(h)); }
+
+int numpmp_gpu_warm_after_degrade(numpmp_gpu* h, const double* cap_before, const double* prior_x,
+                                  const double* prior_lambda_raw, double prior_rho, double* x0_out,
+                                  double* price_out, double* rho_out) {
+  GUARD(h, do_warm_after_degrade(h, cap_before, prior_x, prior_lambda_raw, prior_rho, x0_out,
+                                 price_out, rho_out));
+}
+
+int numpmp_gpu_warm_after_prune(numpmp_gpu* h, const double* x0_proj, const double* price_proj,
+                                double prior_rho, double* x0_out, double* price_out, double* rho_out) {
+  GUARD(h, do_warm_after_prune(h, x0_proj, price_proj, prior_rho, x0_out, price_out, rho_out));
+}
+
+int numpmp_gpu_path_prices(numpmp_gpu* h, const double* lambda, double* pi) {
+  GUARD(h, {
+    if (!lambda || !pi) throw GpuError{NUMPMP_INVALID_ARGUMENT, "path_prices: null array"};
+    upload(h, h->scratch_m2, lambda, 8 * static_cast<size_t>(h->m));
+    k_path_prices<<<grid_for(h->n), 256, 0, h->stream>>>(h->col_ptr, h->row_idx, h->n,
+                                                         h->scratch_m2, h->scratch_n);
+    CK(cudaGetLastError());
+    download(h, pi, h->scratch_n, 8 * static_cast<size_t>(h->n));
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
 
 int numpmp_gpu_set_warm(numpmp_gpu* h, const double* x0, const double* price, double rho) {
   GUARD(h, do_set_warm(h, x0, price, rho));

@@ -256,3 +256,39 @@ def degrade(problem: Problem, p_degrade=0.25, factor=0.5, seed=0) -> Problem:
     if rc:
         raise GenError(L.numpmp_host_last_error().decode())
     return problem.with_capacities(caps)
+
+
+@dataclass
+class PruneMap:  # gen.hpp:146-178
+    link_map: np.ndarray    # old link -> new link or -1 (int32)
+    stream_map: np.ndarray  # old stream -> new stream or -1 (int64)
+
+    def removed_streams(self) -> np.ndarray:
+        return np.nonzero(self.stream_map < 0)[0].astype(np.int64)
+
+    def project_streams(self, v) -> np.ndarray:
+        v = np.asarray(v, np.float64)
+        if v.shape[0] != self.stream_map.shape[0]:
+            raise ValueError("prune map: stream vector length mismatch")
+        return v[self.stream_map >= 0].copy()
+
+    def project_links(self, v) -> np.ndarray:
+        v = np.asarray(v, np.float64)
+        if v.shape[0] != self.link_map.shape[0]:
+            raise ValueError("prune map: link vector length mismatch")
+        return v[self.link_map >= 0].copy()
+
+
+def fail_and_prune(problem: Problem, p_fail=0.25, seed=0):
+    """gen.hpp:181-223 (bit-identical): returns (pruned Problem, PruneMap)."""
+    L = _lib.lib()
+    inst = C.c_void_p()
+    lm = np.empty(problem.m, np.int32)
+    sm = np.empty(problem.n, np.int64)
+    rc = L.numpmp_fail_and_prune(problem.m, problem.n, _lib.ptr(problem.capacities), _lib.ptr(problem.weights),
+                                 _lib.ptr(problem.kinds), _lib.ptr(problem.stream_offsets),
+                                 _lib.ptr(problem.route_links), p_fail, seed, C.byref(inst), _lib.ptr(lm),
+                                 _lib.ptr(sm))
+    if rc:
+        raise GenError(L.numpmp_host_last_error().decode())
+    return _from_instance(inst), PruneMap(lm, sm)

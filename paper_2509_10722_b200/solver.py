@@ -214,6 +214,50 @@ class PmpSolver:
         state.rho, state.iter = new.rho, new.iter
         return r.value, s.value
 
+    # ------------------------------------------- warm-start recipes (warm.hpp)
+    def warm_start_after_degrade(self, before: "Problem", prior: Solution) -> WarmStart:
+        """warm.hpp:25-57 computed on the device for this solver's (degraded)
+        problem; the warm state is applied, so solve_prepared() continues
+        from it.  Returns the recipe's WarmStart."""
+        p = self._problem
+        if before.m != p.m or before.n != p.n:
+            raise ValueError("degrade warm start: problems differ in structure")
+        x0, price, rho = np.empty(p.n), np.empty(p.m), C.c_double()
+        cap_b = np.ascontiguousarray(before.capacities, np.float64)
+        px = np.ascontiguousarray(prior.x, np.float64)
+        pl = np.ascontiguousarray(prior.lambda_raw, np.float64)
+        _check(self._h, _lib.lib().numpmp_gpu_warm_after_degrade(
+            self._h, _lib.ptr(cap_b), _lib.ptr(px), _lib.ptr(pl), float(prior.rho_final), _lib.ptr(x0),
+            _lib.ptr(price), C.byref(rho)))
+        return WarmStart(x0, price, rho.value)
+
+    def warm_start_after_prune(self, prune_map, prior: Solution) -> WarmStart:
+        """warm.hpp:62-94 on the device for this solver's (pruned) problem;
+        the projection onto the survivors is the PruneMap's host gather."""
+        p = self._problem
+        x0p = prune_map.project_streams(prior.x)
+        prp = prune_map.project_links(prior.lambda_raw)
+        if x0p.shape[0] != p.n or prp.shape[0] != p.m:
+            raise ValueError("prune warm start: map does not fit problem")
+        x0, price, rho = np.empty(p.n), np.empty(p.m), C.c_double()
+        _check(self._h, _lib.lib().numpmp_gpu_warm_after_prune(
+            self._h, _lib.ptr(x0p), _lib.ptr(prp), float(prior.rho_final), _lib.ptr(x0), _lib.ptr(price),
+            C.byref(rho)))
+        return WarmStart(x0, price, rho.value)
+
+    def path_prices(self, lam) -> np.ndarray:
+        """transit.hpp:290-302 on the device (route-order sums)."""
+        lam = np.ascontiguousarray(lam, np.float64)
+        if lam.shape[0] != self._problem.m:
+            raise ValueError("path_prices: lambda length mismatch")
+        pi = np.empty(self._problem.n)
+        _check(self._h, _lib.lib().numpmp_gpu_path_prices(self._h, _lib.ptr(lam), _lib.ptr(pi)))
+        return pi
+
+    def solve_prepared(self) -> Solution:
+        """run() from the state the last warm-start recipe applied."""
+        return self._run()
+
     # ----------------------------------------------------------------- solve
     def solve(self, warm: Optional[WarmStart] = None) -> Solution:
         """solver.hpp:411-413 + run 441-508, entirely on the device."""

@@ -624,3 +624,77 @@ def test_p2p_exchange_over_cuda_ipc_processes(restatement, oracle_mod):
     for got, want in [(x, ref.x), (res[0][3], ref.lambda_raw)]:
         ok, err = close(got, want)
         assert ok, err
+
+
+# ------------------------------------------------ warm-start recipes (warm.hpp)
+def test_device_degrade_recipe_matches_reference(reference):
+    # warm.hpp:25-57 on the device == the reference recipe, bit for bit; then
+    # the warm re-solve matches the reference's warm re-solve
+    case = (500, 2000, 6.0, 2, True, 17)
+    base = _gen(*case)
+    deg = pmp.degrade(base, 0.5, 0.5, 99)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1.0)
+    with pmp.PmpSolver(base, cfg) as s:
+        prior = s.solve()
+    rb = reference.build_problem(base.m, base.n, base.stream_offsets, base.route_links, base.kinds, base.weights,
+                                 base.capacities)
+    rd = reference.build_problem(deg.m, deg.n, deg.stream_offsets, deg.route_links, deg.kinds, deg.weights,
+                                 deg.capacities)
+
+    class Prior:
+        x, lambda_raw, rho_final = prior.x, prior.lambda_raw, prior.rho_final
+
+    rx0, rprice, rrho = rb.warm_after_degrade(rd, Prior)
+    with pmp.PmpSolver(deg, cfg) as s:
+        w = s.warm_start_after_degrade(base, prior)
+        sol = s.solve_prepared()
+    np.testing.assert_array_equal(w.x0, rx0)
+    np.testing.assert_array_equal(w.price, rprice)
+    assert w.rho == rrho
+    import oracle.oracle as o
+
+    ref = rd.solve(o.Config(eps_abs=1e-5, rho0=1.0), warm=(rx0, rprice, rrho))
+    assert sol.iterations == ref.iterations
+    ok, err = close(sol.x, ref.x)
+    assert ok, err
+
+
+def test_device_prune_recipe_matches_reference(reference):
+    # warm.hpp:62-94: loads summed in the reference's order, path prices in
+    # route order: the recipe is bit-exact; the warm re-solve agrees
+    case = (500, 2000, 4.0, 2, True, 23)
+    base = _gen(*case)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1.0)
+    with pmp.PmpSolver(base, cfg) as s:
+        prior = s.solve()
+    pruned, pmap = pmp.fail_and_prune(base, 0.2, 4)
+    rb = reference.build_problem(base.m, base.n, base.stream_offsets, base.route_links, base.kinds, base.weights,
+                                 base.capacities)
+    rpr = rb.fail_and_prune(0.2, 4)
+
+    class Prior:
+        x, lambda_raw, rho_final = prior.x, prior.lambda_raw, prior.rho_final
+
+    rx0, rprice, rrho = rpr.warm_after_prune(Prior, base.n, base.m)
+    with pmp.PmpSolver(pruned, cfg) as s:
+        w = s.warm_start_after_prune(pmap, prior)
+        sol = s.solve_prepared()
+    np.testing.assert_array_equal(w.x0, rx0)
+    np.testing.assert_array_equal(w.price, rprice)
+    assert w.rho == rrho
+    import oracle.oracle as o
+
+    ref = rpr.solve(o.Config(eps_abs=1e-5, rho0=1.0), warm=(rx0, rprice, rrho))
+    assert sol.iterations == ref.iterations
+    ok, err = close(sol.x, ref.x)
+    assert ok, err
+
+
+def test_device_path_prices_bit_exact():
+    # transit.hpp:290-302 in route order
+    p, _ = pmp.gen_transit(pmp.TransitSpec(12, 24, 5.0, 40, 30, 3, 6, 50.0, 2))
+    lam = np.random.default_rng(0).uniform(0.0, 2.0, p.m)
+    with pmp.PmpSolver(p, pmp.SolverConfig()) as s:
+        pi = s.path_prices(lam)
+    want = np.array([sum(float(lam[l]) for l in p.route(j)) for j in range(p.n)])
+    np.testing.assert_array_equal(pi, want)

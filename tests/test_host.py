@@ -85,6 +85,21 @@ def test_degrade_bit_exact(reference):
     np.testing.assert_array_equal(p.capacities, rd.capacities)
 
 
+@pytest.mark.parametrize("p_fail,seed", [(0.25, 0), (0.1, 9)])
+def test_fail_and_prune_bit_exact(reference, p_fail, seed):
+    # gen.hpp:181-223 and the PruneMap of gen.hpp:146-178
+    case = (400, 1500, 4.0, 2, ("uniform", 0.5, 1.5), 5)
+    rp = reference.gen(*case).fail_and_prune(p_fail, seed)
+    ra = rp.arrays()
+    lm, sm = rp.prune_maps()
+    q, mp = pmp.fail_and_prune(pmp.gen_uncongested(_spec(*case)), p_fail, seed)
+    assert (q.m, q.n, q.nnz) == (rp.m, rp.n, rp.nnz)
+    for mine, theirs in [(q.stream_offsets, ra.stream_offsets), (q.route_links, ra.route_links),
+                         (q.capacities, ra.capacities), (q.weights, ra.weights), (q.kinds, ra.kinds),
+                         (mp.link_map, lm), (mp.stream_map, sm)]:
+        np.testing.assert_array_equal(mine, theirs)
+
+
 @pytest.mark.parametrize("name", ["config_a", "mixed_small", "transit_small"])
 def test_host_layout_matches_golden(name):
     z = np.load(os.path.join(GOLDEN, name + ".npz"))
