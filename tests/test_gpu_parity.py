@@ -696,5 +696,10 @@ def test_device_path_prices_bit_exact():
     lam = np.random.default_rng(0).uniform(0.0, 2.0, p.m)
     with pmp.PmpSolver(p, pmp.SolverConfig()) as s:
         pi = s.path_prices(lam)
-    want = np.array([sum(float(lam[l]) for l in p.route(j)) for j in range(p.n)])
+    want = np.zeros(p.n)
+    for j in range(p.n):  # plain left-to-right adds (Python's sum() compensates since 3.12)
+        t = 0.0
+        for l in p.route(j):
+            t += float(lam[l])
+        want[j] = t
     np.testing.assert_array_equal(pi, want)
