@@ -9,6 +9,8 @@
  *   numpmp_gen_congested    gen.hpp:103-128
  *   numpmp_degrade          gen.hpp:132-143
  *   numpmp_fail_and_prune   gen.hpp:146-223
+ *   numpmp_read_problem     io.hpp:172-279 (parallel decode of NUMPB)
+ *   numpmp_write_problem    io.hpp:126-170
  *   numpmp_validate         model.hpp:76-155 (+ violations_message 203-215)
  *   numpmp_build_layout     model.hpp:159-201
  */
@@ -70,6 +72,15 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
 
 /* In-place capacity degradation with the reference's draw order. */
 int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor, uint64_t seed);
+/* Problem files (io.hpp:126-279): read_problem of the text "NUMP 1" or the
+ * binary "NUMPB 1" container (sniffed by magic) into an instance; returns 0,
+ * 6 (IoError, the reference's message) or 2 (ValidationError from
+ * build_problem).  write_problem: encoding 0 auto (binary when m >= 1e6),
+ * 1 text, 2 binary; the same bytes as the reference writer. */
+int numpmp_read_problem(const char* path, numpmp_instance** out);
+int numpmp_write_problem(int64_t m, int64_t n, const double* capacities, const double* weights,
+                         const uint8_t* kinds, const int64_t* offsets, const int32_t* routes,
+                         const char* path, int encoding);
 /* fail_and_prune (gen.hpp:181-223): the pruned instance plus the PruneMap
  * (gen.hpp:146-178): link_map[m] (new id or -1), stream_map[n] (new id or -1). */
 int numpmp_fail_and_prune(int64_t m, int64_t n, const double* capacities, const double* weights,

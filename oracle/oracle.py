@@ -245,6 +245,8 @@ class Reference:
         L.ref_degrade.argtypes = [P, D, D, C.c_uint64, C.POINTER(P)]
         L.ref_fail_and_prune.argtypes = [P, D, C.c_uint64, C.POINTER(P)]
         L.ref_prune_maps.argtypes = [P, P, P]
+        L.ref_write_problem.argtypes = [P, C.c_char_p, C.c_int]
+        L.ref_read_problem.argtypes = [C.c_char_p, C.POINTER(P)]
         L.ref_build_problem.argtypes = [I64, I64, P, P, P, P, P, C.POINTER(P)]
         L.ref_sizes.argtypes = [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]
         L.ref_free.argtypes = [P]
@@ -284,6 +286,12 @@ class Reference:
         rp = RefProblem(self, h)
         rp.dropped = dropped.value
         return rp
+
+    def read_problem(self, path) -> "RefProblem":
+        """io.hpp:172-279; raises RuntimeError with the reference's message."""
+        h = P()
+        self._err(self.L.ref_read_problem(os.fsencode(path), C.byref(h)))
+        return RefProblem(self, h)
 
     def build_problem(self, m, n, stream_offsets, routes, kinds, weights, capacities) -> "RefProblem":
         h = P()
@@ -331,6 +339,10 @@ class RefProblem:
         self.ref.L.ref_export(self.h, _p(a.capacities), _p(a.weights), _p(a.kinds), _p(a.stream_offsets),
                               _p(a.terminal_link), _p(a.link_offsets), _p(a.link_terminals), _p(a.link_counts))
         return a
+
+    def write_problem(self, path, encoding="auto"):
+        self.ref._err(self.ref.L.ref_write_problem(self.h, os.fsencode(path),
+                                                   {"auto": 0, "text": 1, "binary": 2}[encoding]))
 
     def degrade(self, p_degrade, factor, seed) -> "RefProblem":
         h = P()

@@ -20,6 +20,7 @@
 
 #include "numpmp/common.hpp"
 #include "numpmp/gen.hpp"
+#include "numpmp/io.hpp"
 #include "numpmp/model.hpp"
 #include "numpmp/parallel.hpp"
 #include "numpmp/prox.hpp"
@@ -74,6 +75,33 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 void ref_free(void* h) { delete static_cast<RefProblem*>(h); }
+
+// io.hpp:126-279 (encoding: 0 auto, 1 text, 2 binary)
+int ref_write_problem(void* h, const char* path, int encoding) {
+  try {
+    write_problem(static_cast<RefProblem*>(h)->p, path,
+                  encoding == 1 ? ProblemEncoding::Text
+                                : (encoding == 2 ? ProblemEncoding::Binary : ProblemEncoding::Auto));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int ref_read_problem(const char* path, void** out) {
+  try {
+    auto* r = new RefProblem();
+    try {
+      r->p = read_problem(path);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
 
 // gen.hpp:91-97 / 103-128.  kind: 0 log, 1 linear, 2 mixed;
 // wkind: 0 constant(wa), 1 uniform(wa, wb).  congested != 0 -> gen_congested.

@@ -7,7 +7,7 @@ SolverState / Solution types and PmpSolver members, with every iteration
 running as hand-written CUDA kernels behind the C-ABI in
 include/numpmp_gpu.h.
 """
-from .errors import DeviceError, DomainError, GenError, SolverError, ValidationError
+from .errors import DeviceError, DomainError, GenError, IoError, SolverError, ValidationError
 from .model import (
     GenKind,
     GenSpec,
@@ -25,7 +25,9 @@ from .model import (
     gen_transit,
     gen_uncongested,
     problem_from_arrays,
+    read_problem,
     validate,
+    write_problem,
 )
 from .solver import (
     PmpSolver,
@@ -43,9 +45,9 @@ from .solver import (
 )
 
 __all__ = [
-    "DeviceError", "DomainError", "GenError", "SolverError", "ValidationError",
+    "DeviceError", "DomainError", "GenError", "IoError", "SolverError", "ValidationError",
     "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitSpec", "WeightDist",
-    "build_problem", "degrade", "fail_and_prune", "PruneMap", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "validate",
+    "build_problem", "degrade", "fail_and_prune", "PruneMap", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "read_problem", "validate", "write_problem",
     "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
     "check_termination", "objective", "recover_duals", "to_string", "update_rho",
 ]

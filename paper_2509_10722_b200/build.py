@@ -12,8 +12,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_DIR = os.path.join(HERE, "lib")
 OUT = os.path.join(LIB_DIR, "libnumpmp_cuda.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("pmp_solver.cu", "host_gen.cpp")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pmp_kernels.cuh", "pmp_aux.cuh")] + [
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("pmp_solver.cu", "host_gen.cpp", "host_io.cpp")]
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pmp_kernels.cuh", "pmp_aux.cuh", "pmp_p2p.cuh",
+                                                            "host_instance.h")] + [
     os.path.join(ROOT, "include", f) for f in ("numpmp_gpu.h", "numpmp_host.h")
 ]
 NVCC_FLAGS = [

@@ -27,10 +27,11 @@
 #include <vector>
 
 #include "numpmp_host.h"
+#include "host_instance.h"
+
+thread_local std::string g_host_err;  // declared in host_instance.h
 
 namespace {
-
-thread_local std::string g_host_err;
 
 // rng.hpp:17-77, draw for draw.
 class Rng {
@@ -95,13 +96,7 @@ class Rng {
 
 }  // namespace
 
-struct numpmp_instance {
-  std::int64_t m = 0, n = 0;
-  std::vector<double> capacities, weights;
-  std::vector<std::uint8_t> kinds;
-  std::vector<std::int64_t> offsets;
-  std::vector<std::int32_t> routes;
-};
+
 
 namespace {
 

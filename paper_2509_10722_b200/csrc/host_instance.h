@@ -1,0 +1,19 @@
+// host_instance.h -- the library-owned instance behind numpmp_instance*
+// (numpmp_host.h): flat stream-major incidence, shared by the generators
+// (host_gen.cpp) and the problem-file reader (host_io.cpp).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+struct numpmp_instance {
+  std::int64_t m = 0, n = 0;
+  std::vector<double> capacities, weights;
+  std::vector<std::uint8_t> kinds;
+  std::vector<std::int64_t> offsets;
+  std::vector<std::int32_t> routes;
+};
+
+// Message of the last failing host call (numpmp_host_last_error), per thread.
+extern thread_local std::string g_host_err;

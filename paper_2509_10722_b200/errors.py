@@ -14,6 +14,10 @@ class GenError(RuntimeError):
     """Invalid generator specification (common.hpp:38-43)."""
 
 
+class IoError(RuntimeError):
+    """Problem / solution file errors (common.hpp:32-36)."""
+
+
 class DomainError(ValueError):
     """std::domain_error (e.g. warm start with a non-positive log rate)."""
 

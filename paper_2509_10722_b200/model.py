@@ -12,6 +12,7 @@ libnumpmp_cuda.so (csrc/host_gen.cpp).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import List, Optional, Sequence
@@ -292,3 +293,30 @@ def fail_and_prune(problem: Problem, p_fail=0.25, seed=0):
     if rc:
         raise GenError(L.numpmp_host_last_error().decode())
     return _from_instance(inst), PruneMap(lm, sm)
+
+
+def read_problem(path: str) -> Problem:
+    """io.hpp:172-279: text "NUMP 1" or binary "NUMPB 1" (by magic)."""
+    from .errors import IoError, ValidationError
+
+    L = _lib.lib()
+    inst = C.c_void_p()
+    rc = L.numpmp_read_problem(os.fsencode(path), C.byref(inst))
+    if rc == 2:
+        raise ValidationError(L.numpmp_host_last_error().decode())
+    if rc:
+        raise IoError(L.numpmp_host_last_error().decode())
+    return _from_instance(inst)
+
+
+def write_problem(problem: Problem, path: str, encoding: str = "auto") -> None:
+    """io.hpp:126-170 (encoding: "auto" | "text" | "binary")."""
+    from .errors import IoError
+
+    L = _lib.lib()
+    enc = {"auto": 0, "text": 1, "binary": 2}[encoding]
+    rc = L.numpmp_write_problem(problem.m, problem.n, _lib.ptr(problem.capacities), _lib.ptr(problem.weights),
+                                _lib.ptr(problem.kinds), _lib.ptr(problem.stream_offsets),
+                                _lib.ptr(problem.route_links), os.fsencode(path), enc)
+    if rc:
+        raise IoError(L.numpmp_host_last_error().decode())

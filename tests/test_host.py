@@ -3,6 +3,7 @@ validation and the reference layout (csrc/host_gen.cpp), each bit-exact
 against the reference (oracle/_ref) or the committed golden fixtures, and
 the multi-GPU shard partition."""
 import os
+import struct
 
 import numpy as np
 import pytest
@@ -179,3 +180,70 @@ def test_shard_bounds_tile_and_balance(world):
     assert [s0 for _, s0 in parts] == list(b[:-1])
     for q, _ in parts:
         assert q.stream_offsets[0] == 0 and q.m == p.m
+
+
+# ------------------------------------------------------ problem files (io.hpp)
+@pytest.mark.parametrize("encoding", ["text", "binary"])
+def test_problem_files_match_reference(reference, tmp_path, encoding):
+    # io.hpp:126-279: the reference's file read by ours gives its Problem,
+    # and ours writes the reference's bytes
+    case = (400, 1500, 4.0, 2, ("uniform", 0.5, 1.5), 5)
+    rp = reference.gen(*case)
+    ra = rp.arrays()
+    f_ref = str(tmp_path / ("ref." + encoding))
+    rp.write_problem(f_ref, encoding)
+    q = pmp.read_problem(f_ref)
+    nnz = int(ra.stream_offsets[-1])
+    for mine, theirs in [(q.stream_offsets, ra.stream_offsets), (q.route_links, ra.terminal_link[:nnz]),
+                         (q.capacities, ra.capacities), (q.weights, ra.weights), (q.kinds, ra.kinds)]:
+        np.testing.assert_array_equal(mine, theirs)
+    f_ours = str(tmp_path / ("ours." + encoding))
+    pmp.write_problem(q, f_ours, encoding)
+    assert open(f_ours, "rb").read() == open(f_ref, "rb").read()
+
+
+BAD_FILES = [
+    b"NUMP 2 1 1\n1\nlog 1 1 0\n",
+    b"NUMP 1 2 1\n1\nlog 1 1 0\n",
+    b"NUMP 1 1 1\n1.5x\nlog 1 1 0\n",
+    b"NUMP 1 1 1\n1\nfoo 1 1 0\n",
+    b"NUMP 1 1 1\n1\nlog 1 2 0\n",
+    b"NUMP 1 1 2\n1\nlog 1 1 0\n",
+    b"NUMP 1 1 1\n1\nlog 1 1 0\n\nlog 1 1 0\n",
+    b"NUMP 1 1 1\n1\nlog 1\n",
+    b"NUMP 1 0 1\n",
+    b"NUMP 1 2 1\n1 1\nlog 1 2 0 0\n",       # duplicate link: ValidationError
+    b"NUMP 1 1 1\n-1\nlog 1 1 0\n",          # capacity <= 0: ValidationError
+    b"NUMPB 1\n\x01\x00\x00\x00\x00\x00\x00\x00",  # truncated header
+    b"NUMPB 1\n" + (1).to_bytes(8, "little") + (1).to_bytes(8, "little") + struct.pack("<d", 1.0)
+    + b"\x07",  # unknown kind
+    b"NUMPB 1\n" + (1).to_bytes(8, "little") + (1).to_bytes(8, "little") + struct.pack("<d", 1.0)
+    + b"\x00" + struct.pack("<d", 1.0) + (3).to_bytes(8, "little") + (0).to_bytes(8, "little"),  # truncated route
+]
+
+
+@pytest.mark.parametrize("blob", BAD_FILES)
+def test_problem_file_errors_match_reference(reference, tmp_path, blob):
+    f = str(tmp_path / "bad.nump")
+    open(f, "wb").write(blob)
+    with pytest.raises(RuntimeError) as theirs:
+        reference.read_problem(f)
+    with pytest.raises((pmp.IoError, pmp.ValidationError)) as mine:
+        pmp.read_problem(f)
+    assert str(theirs.value).split(": ", 1)[1] == str(mine.value)
+
+
+@pytest.mark.slow
+def test_binary_reader_config_c_scale(tmp_path):
+    # the reference reads config C in 11.9 s single-threaded
+    import time
+
+    p = pmp.gen_uncongested(_spec(1000000, 10000000, 10.0, 2, ("uniform", 0.5, 1.5), 7))
+    f = str(tmp_path / "c.numpb")
+    pmp.write_problem(p, f, "binary")
+    t = time.perf_counter()
+    q = pmp.read_problem(f)
+    dt = time.perf_counter() - t
+    np.testing.assert_array_equal(q.route_links, p.route_links)
+    np.testing.assert_array_equal(q.stream_offsets, p.stream_offsets)
+    print(f"read_problem config C: {dt:.2f} s")
