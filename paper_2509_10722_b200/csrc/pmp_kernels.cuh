@@ -642,8 +642,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   last_block_finalize(a, rho, gridDim.x, false);
 }
 
-// Sharded: the replicated link epilogue on the all-reduced loads Lbuf (one
-// thread per link), residual partials, last-CTA finalize.
+// The link epilogue as a streaming pass (one thread per link, coalesced):
+// kSrc 0 = sharded, on the all-reduced loads Lbuf (scalars in Lbuf[m..]);
+// kSrc 1 = one device, on the loads the last block accumulated into Lacc.
+// Residual partials, last-CTA finalize.
+template <int kSrc>
 __global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
   __shared__ bool s_last;
   if (kernel_should_exit(a.ctrl)) return;
@@ -651,16 +654,17 @@ __global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
   double part[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* L = (kSrc == 0) ? a.Lbuf : a.Lacc;
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.m;
        r += (long long)gridDim.x * blockDim.x)
-    link_epilogue(a, r, __ldcg(a.Lbuf + r), __ldg(a.deg + r), rho, part, pol_first, pol_last);
+    link_epilogue(a, r, __ldcg(L + r), __ldg(a.deg + r), rho, part, pol_first, pol_last);
   block_sum_store<4>(part, a.k2_part + 4 * blockIdx.x);
   __threadfence();
   if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket, 1u) == gridDim.x - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  last_block_finalize(a, rho, gridDim.x, true);
+  last_block_finalize(a, rho, gridDim.x, kSrc == 0);
 }
 
 }  // namespace numpmp_dev

@@ -154,6 +154,10 @@ struct ColBlock {
 struct numpmp_gpu {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // side stream of the pipelined graph (stream passes)
+  cudaEvent_t pipe_ev[2 * kMaxBlocks + 2] = {};
+  bool split_epilogue = false;     // NUMPMP_SPLIT_EPILOGUE: streaming epilogue kernel
+  bool pipeline = false;           // NUMPMP_PIPELINE: K1(b+1) overlaps K2(b)
   std::string err;
   numpmp_config cfg{};
   int64_t m = 0, n = 0, nnz = 0;
@@ -229,7 +233,7 @@ struct numpmp_gpu {
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
   int launches_per_iteration() const {
-    return p2p ? 2 * nb() + 5 : 1 + 2 * nb() + (sharded ? 1 : 0);
+    return p2p ? 2 * nb() + 5 : 1 + 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
   }
   std::vector<int> launch_side;  // per launch of an iteration: 1 stream side, 2 link side
 };
@@ -382,7 +386,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
     mark(1);
-    if (b + 1 < nb)
+    if (b + 1 < nb || (h->split_epilogue && !h->sharded))
       k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else if (h->p2p)
       k_link_pass<LP_P2P><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
@@ -402,10 +406,48 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
   } else if (h->sharded) {
     NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum, h->comm,
                  h->stream));
-    k_link_epilogue<<<h->grid3, kThreads, 0, h->stream>>>(a);
+    k_link_epilogue<0><<<h->grid3, kThreads, 0, h->stream>>>(a);
+    mark(2);
+  } else if (h->split_epilogue) {
+    k_link_epilogue<1><<<h->grid3, kThreads, 0, h->stream>>>(a);
     mark(2);
   }
   h->launch_side = side;
+}
+
+// The same iteration with the stream passes on a side stream: K1(b+1) may
+// run while K2(b) drains (filling its tail), K1(b+2) waits for K2(b) so at
+// most two x blocks are live in L2.  Launch order, work split and summation
+// order are unchanged, so results are bit-identical to the serial graph.
+// Single device only; used for graphs without per-launch events.
+void enqueue_iteration_pipelined(numpmp_gpu* h, int parity, int mode) {
+  IterArgs a = make_args(h, parity, mode);
+  const int nb = h->nb();
+  cudaEvent_t* ev_k1 = h->pipe_ev;            // [nb]: K1(b) done
+  cudaEvent_t* ev_k2 = h->pipe_ev + kMaxBlocks;  // [nb]: K2(b) done
+  cudaEvent_t ev_start = h->pipe_ev[2 * kMaxBlocks];
+  k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ev_start, h->stream));
+  CK(cudaStreamWaitEvent(h->stream2, ev_start, 0));
+  for (int b = 0; b < nb; ++b) {
+    const BlockArgs bk = block_args(h, b);
+    if (b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
+    k_stream_pass<<<h->grid1, kThreads, 0, h->stream2>>>(a, bk);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev_k1[b], h->stream2));
+    CK(cudaStreamWaitEvent(h->stream, ev_k1[b], 0));
+    if (b + 1 < nb || h->split_epilogue)
+      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+    else
+      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev_k2[b], h->stream));
+  }
+  if (h->split_epilogue) {
+    k_link_epilogue<1><<<h->grid3, kThreads, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+  }
 }
 
 cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
@@ -414,10 +456,14 @@ cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
   const size_t set_base = ev_set < 0 ? 0 : static_cast<size_t>(ev_set) * (kBatchIters * lpi + 1);
   CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    for (int i = 0; i < kBatchIters; ++i)
-      enqueue_iteration(h, parity ^ (i & 1), MODE_RUN,
-                        ev_set >= 0 ? &h->prof_ev[set_base + static_cast<size_t>(i * lpi)] : nullptr,
-                        i == 0);
+    for (int i = 0; i < kBatchIters; ++i) {
+      if (h->pipeline && ev_set < 0 && !h->sharded)
+        enqueue_iteration_pipelined(h, parity ^ (i & 1), MODE_RUN);
+      else
+        enqueue_iteration(h, parity ^ (i & 1), MODE_RUN,
+                          ev_set >= 0 ? &h->prof_ev[set_base + static_cast<size_t>(i * lpi)] : nullptr,
+                          i == 0);
+    }
   } catch (...) {
     cudaStreamEndCapture(h->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -666,6 +712,10 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaSetDevice(h->device));
   keep_pool_memory(h->device);
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : h->pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (const char* env = std::getenv("NUMPMP_SPLIT_EPILOGUE")) h->split_epilogue = std::atoi(env) != 0;
+  if (const char* env = std::getenv("NUMPMP_PIPELINE")) h->pipeline = std::atoi(env) != 0;
   pt.mark("create: stream");
   const int64_t m = h->m, n = h->n, nnz = h->nnz;
   int64_t* b = &h->dev_bytes;
@@ -765,7 +815,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
   int occ3 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
   int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
@@ -1681,6 +1731,9 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     }
   if (h->ctrl_host) cudaFreeHost(h->ctrl_host);
   if (h->comm) nccl().CommDestroy(h->comm);
+  for (cudaEvent_t e : h->pipe_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream2) cudaStreamDestroy(h->stream2);
   if (h->stream) {
     cudaStreamSynchronize(h->stream);
     cudaStreamDestroy(h->stream);
