@@ -156,8 +156,8 @@ struct numpmp_gpu {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // side stream of the pipelined graph (stream passes)
   cudaEvent_t pipe_ev[2 * kMaxBlocks + 2] = {};
-  bool split_epilogue = false;     // NUMPMP_SPLIT_EPILOGUE: streaming epilogue kernel
-  bool pipeline = false;           // NUMPMP_PIPELINE: K1(b+1) overlaps K2(b)
+  bool split_epilogue = true;      // NUMPMP_SPLIT_EPILOGUE=0: epilogue fused into the last link pass
+  bool pipeline = true;            // NUMPMP_PIPELINE=0: serial graph (K1(b+1) no longer overlaps K2(b))
   std::string err;
   numpmp_config cfg{};
   int64_t m = 0, n = 0, nnz = 0;
@@ -716,6 +716,14 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   for (cudaEvent_t& e : h->pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* env = std::getenv("NUMPMP_SPLIT_EPILOGUE")) h->split_epilogue = std::atoi(env) != 0;
   if (const char* env = std::getenv("NUMPMP_PIPELINE")) h->pipeline = std::atoi(env) != 0;
+  // L2 set-aside for the evict_last lines (x of the live column blocks, v):
+  // NUMPMP_L2_PERSIST_MB (default 0: the driver default).
+  if (const char* env = std::getenv("NUMPMP_L2_PERSIST_MB")) {
+    const size_t want = static_cast<size_t>(std::atoll(env)) << 20;
+    int dev_max = 0;
+    CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxPersistingL2CacheSize, h->device));
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(want, static_cast<size_t>(dev_max))));
+  }
   pt.mark("create: stream");
   const int64_t m = h->m, n = h->n, nnz = h->nnz;
   int64_t* b = &h->dev_bytes;
