@@ -717,12 +717,19 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   if (const char* env = std::getenv("NUMPMP_SPLIT_EPILOGUE")) h->split_epilogue = std::atoi(env) != 0;
   if (const char* env = std::getenv("NUMPMP_PIPELINE")) h->pipeline = std::atoi(env) != 0;
   // L2 set-aside for the evict_last lines (x of the live column blocks, v):
-  // NUMPMP_L2_PERSIST_MB (default 0: the driver default).
-  if (const char* env = std::getenv("NUMPMP_L2_PERSIST_MB")) {
-    const size_t want = static_cast<size_t>(std::atoll(env)) << 20;
-    int dev_max = 0;
-    CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxPersistingL2CacheSize, h->device));
-    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(want, static_cast<size_t>(dev_max))));
+  // 32 MB measured best at config C (profiles/r1_l2_sweep.txt);
+  // NUMPMP_L2_PERSIST_MB overrides (0 = leave the device limit alone).
+  {
+    size_t want = size_t(32) << 20;
+    if (const char* env = std::getenv("NUMPMP_L2_PERSIST_MB")) want = static_cast<size_t>(std::atoll(env)) << 20;
+    if (want > 0) {
+      int dev_max = 0;
+      CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxPersistingL2CacheSize, h->device));
+      size_t cur = 0;
+      CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+      const size_t set = std::min<size_t>(want, static_cast<size_t>(dev_max));
+      if (cur != set) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set));
+    }
   }
   pt.mark("create: stream");
   const int64_t m = h->m, n = h->n, nnz = h->nnz;
