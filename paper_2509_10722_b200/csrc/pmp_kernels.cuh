@@ -88,6 +88,7 @@ struct Ctrl {
   unsigned ticket;   // last-block detection, link pass
   unsigned ticket2;  // last-block detection, sharded gather pass
   unsigned ticket3;  // last-block detection, peer-memory owner epilogue
+  int v_sel;         // v of the next iteration: 0 v, 1 v_alt[0] (rho*gamma), 2 v_alt[1] (rho/gamma)
 };
 
 // Peer-memory exchange of the sharded engine (pmp_p2p.cuh).  Links are
@@ -136,6 +137,10 @@ struct IterArgs {
   const double* Q_in;
   double* Q_out;
   double* v;
+  // On rho-update iterations (k % rho_update_interval == 0) the link
+  // epilogue also writes v for both candidate rhos; finalize_iteration
+  // selects one (Ctrl::v_sel), so no pass rebuilds v after a rho change.
+  double* v_alt[2];
   double* k1_part;  // [nb][grid1][2]: tau dA^2, objective
   double* k2_part;  // [grid2][4]: r^2, dB.dQ, d dB^2, dzs^2
   int grid1, grid2, grid3, nblocks;
@@ -339,7 +344,7 @@ __device__ __forceinline__ bool kernel_should_exit(const Ctrl* ctrl) {
 // (rho_changed, set by finalize_iteration / the host): recompute it before
 // the iteration's first stream pass.  Exits at entry otherwise.
 __global__ void __launch_bounds__(kThreads) k_refresh_v(IterArgs a) {
-  if (kernel_should_exit(a.ctrl) || a.ctrl->rho_changed == 0) return;
+  if (a.ctrl->rho_changed == 0) return;
   const double rho = a.ctrl->rho;
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < a.m;
        l += (long long)gridDim.x * blockDim.x)
@@ -398,7 +403,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   const bool trace_it = (a.mode == MODE_RUN) && (k % a.trace_every == 0);
   double part[2] = {0.0, 0.0};
   int* sb = sidx[threadIdx.x >> 5];
-  stream_pass_body(a, bk, GatherV{a.v}, rho, trace_it, sb, part[0], part[1]);
+  const int sel = a.ctrl->v_sel;
+  const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
+  stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 
@@ -435,6 +442,11 @@ __device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, 
   a.pr_out[r] = prn;
   const double vn = Bn + prn / rho;
   st_hint_f64(a.v + r, vn, pol_last);
+  if (a.v_alt[0] != nullptr && a.mode == MODE_RUN && (a.ctrl->run_k + 1) % a.rho_interval == 0) {
+    // the rhos finalize_iteration may switch to, computed as it does
+    st_hint_f64(a.v_alt[0] + r, Bn + prn / (rho * a.gamma), pol_last);
+    st_hint_f64(a.v_alt[1] + r, Bn + prn / (rho / a.gamma), pol_last);
+  }
   return vn;
 }
 
@@ -452,6 +464,7 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
   c->r_norm = r_norm;
   c->s_norm = s_norm;
   c->rho_changed = 0;
+  c->v_sel = 0;
   if (a.mode != MODE_RUN) return;  // step(): no control (solver.hpp:318-409)
   const long long k = ++c->run_k;
   if (!isfinite(r_norm) || !isfinite(s_norm)) {
@@ -482,9 +495,11 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
     if (r_norm > a.mu * s_norm) {
       c->rho = rho * a.gamma;
       c->rho_changed = 1;
+      c->v_sel = 1;
     } else if (s_norm > a.mu * r_norm) {
       c->rho = rho / a.gamma;
       c->rho_changed = 1;
+      c->v_sel = 2;
     }
   }
   if (k >= a.max_iters) {

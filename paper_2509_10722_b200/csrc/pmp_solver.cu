@@ -195,6 +195,7 @@ struct numpmp_gpu {
   double* Q[2] = {nullptr, nullptr};
   double* x = nullptr;
   double* v = nullptr;
+  double* v_alt[2] = {nullptr, nullptr};  // v for rho*gamma, rho/gamma (rho-update iterations)
   double* ps0 = nullptr;    // slack flows of an uploaded state
   double* pbar0 = nullptr;  // link averages of an uploaded state
   double* Lbuf = nullptr;   // m + 2
@@ -233,7 +234,7 @@ struct numpmp_gpu {
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
   int launches_per_iteration() const {
-    return p2p ? 2 * nb() + 5 : 1 + 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
+    return p2p ? 2 * nb() + 5 : 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
   }
   std::vector<int> launch_side;  // per launch of an iteration: 1 stream side, 2 link side
 };
@@ -321,6 +322,8 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.Q_in = h->Q[i];
   a.Q_out = h->Q[o];
   a.v = h->v;
+  a.v_alt[0] = h->p2p ? nullptr : h->v_alt[0];
+  a.v_alt[1] = h->p2p ? nullptr : h->v_alt[1];
   a.k1_part = h->k1_part;
   a.k2_part = h->k2_part;
   a.grid1 = h->grid1;
@@ -378,9 +381,6 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     mark(1);
     k_p2p_wait<2, 1><<<1, 32, 0, h->stream>>>(a);
     mark(1);
-  } else {
-    k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
-    mark(1);
   }
   for (int b = 0; b < nb; ++b) {
     const BlockArgs bk = block_args(h, b);
@@ -426,8 +426,6 @@ void enqueue_iteration_pipelined(numpmp_gpu* h, int parity, int mode) {
   cudaEvent_t* ev_k1 = h->pipe_ev;            // [nb]: K1(b) done
   cudaEvent_t* ev_k2 = h->pipe_ev + kMaxBlocks;  // [nb]: K2(b) done
   cudaEvent_t ev_start = h->pipe_ev[2 * kMaxBlocks];
-  k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
-  CK(cudaGetLastError());
   CK(cudaEventRecord(ev_start, h->stream));
   CK(cudaStreamWaitEvent(h->stream2, ev_start, 0));
   for (int b = 0; b < nb; ++b) {
@@ -749,6 +747,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   }
   h->x = dalloc<double>(static_cast<size_t>(n), b, h->stream);
   h->v = dalloc<double>(static_cast<size_t>(m), b, h->stream);
+  for (int i = 0; i < 2; ++i) h->v_alt[i] = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->ps0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->pbar0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b, h->stream);
@@ -864,6 +863,10 @@ void reset_ctrl(numpmp_gpu* h, double rho, int64_t iter) {
   c.rho_changed = 1;  // k_refresh_v builds v from B and price
   std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
   CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+  if (!h->p2p) {  // v = B + price / rho of the uploaded state (the peer-memory path refreshes in-graph)
+    k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(make_args(h, h->cur, MODE_AUX));
+    CK(cudaGetLastError());
+  }
   CK(cudaStreamSynchronize(h->stream));
 }
 
@@ -1718,6 +1721,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
                              h->done_cnt, h->ep_part, h->k1_scalars, h->peer_tables,
+                             h->v_alt[0], h->v_alt[1],
                              h->Lbuf,    h->Lacc,    h->k1_part,   h->k2_part,    h->scratch_m,
                              h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
   for (int i = 0; i < 2; ++i) {

@@ -24,16 +24,20 @@ def val(d, m):
 per = {}
 for d in data:
     name = d[ix["Kernel Name"]].split("(")[0].replace("void ", "").split("<")[0].replace("numpmp_dev::", "")
-    key = "k_stream_pass" if "stream_pass" in name else "k_link_pass"
+    # stream side: the stream passes (+ the v refresh they wait for); link side:
+    # the link passes and the link epilogue
+    key = "k_stream_pass" if ("stream_pass" in name or "refresh_v" in name) else "k_link_pass"
     e = per.setdefault(key, {"dram_bytes": 0.0, "ncu_us": 0.0, "launches": 0, "xbar_req_pct": [], "l2_hit_pct": []})
     e["dram_bytes"] += val(d, "dram__bytes_read.sum") + val(d, "dram__bytes_write.sum")
     e["ncu_us"] += float(d[ix["gpu__time_duration.sum"]]) / (1e3 if units[ix["gpu__time_duration.sum"]] == "nsecond" else 1.0)
     e["launches"] += 1
-    e["xbar_req_pct"].append(float(d[ix["l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"]]))
-    e["l2_hit_pct"].append(float(d[ix["lts__t_sector_hit_rate.pct"]]))
-for e in per.values():
-    e["xbar_req_pct"] = round(sum(e["xbar_req_pct"]) / len(e["xbar_req_pct"]), 1)
-    e["l2_hit_pct"] = round(sum(e["l2_hit_pct"]) / len(e["l2_hit_pct"]), 1)
+    t_us = float(d[ix["gpu__time_duration.sum"]]) / (1e3 if units[ix["gpu__time_duration.sum"]] == "nsecond" else 1.0)
+    e["xbar_req_pct"].append((t_us, float(d[ix["l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"]])))
+    e["l2_hit_pct"].append((t_us, float(d[ix["lts__t_sector_hit_rate.pct"]])))
+for e in per.values():  # time-weighted over the launches of the iteration
+    for k in ("xbar_req_pct", "l2_hit_pct"):
+        tot = sum(t for t, _ in e[k])
+        e[k] = round(sum(t * v for t, v in e[k]) / tot, 1) if tot > 0 else None
     e["ncu_us"] = round(e["ncu_us"], 1)
 print(json.dumps({"source": f"{rep} (ncu --set full --clock-control none, scripts/profile_run.py {cfg}; one iteration)",
                   "config": cfg, "per_iteration": per}, indent=1))
