@@ -8,7 +8,7 @@ build() {  # name, extra nvcc flags...
   local name=$1; shift
   nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -shared \
     -Iinclude "$@" -o build/variants/lib_$name.so \
-    paper_2509_10722_b200/csrc/pmp_solver.cu paper_2509_10722_b200/csrc/host_gen.cpp -ldl -cudart static &
+    paper_2509_10722_b200/csrc/pmp_solver.cu paper_2509_10722_b200/csrc/host_gen.cpp paper_2509_10722_b200/csrc/host_io.cpp -ldl -cudart static &
 }
 build base
 build u4_minb6 -DNUMPMP_GATHER_UNROLL=4 -DNUMPMP_MIN_BLOCKS=6
