@@ -703,3 +703,51 @@ def test_device_path_prices_bit_exact():
             t += float(lam[l])
         want[j] = t
     np.testing.assert_array_equal(pi, want)
+
+
+# ------------------------------------------- skew, ragged routes, edge shapes
+def _ragged_problem():
+    # one stream over every link (a 700-link route spans several staging
+    # rounds of its tile), single-link routes, and links nobody uses
+    rng = np.random.default_rng(5)
+    m = 700
+    routes = [list(range(m))]
+    for j in range(1, 2000):
+        k = 1 if j % 3 == 0 else int(rng.integers(2, 9))
+        routes.append(sorted(rng.choice(600, size=k, replace=False).tolist()))  # links 600..699: only stream 0
+    S = pmp.Stream
+    streams = [S(j, pmp.StreamKind.Log if j % 2 else pmp.StreamKind.Linear, "", float(rng.uniform(0.5, 1.5)), r)
+               for j, r in enumerate(routes)]
+    return pmp.build_problem(streams, rng.uniform(0.5, 1.5, m).tolist())
+
+
+SHAPE_CASES = {
+    # hot links: 10 links in ~10% of the streams each (rows of ~2000 entries,
+    # segment bound raised above 16 so a row still fits one warp unit)
+    "congested": lambda: pmp.gen_congested(pmp.GenSpec(m=2000, n=20000, avg_links_per_stream=4.0,
+                                                       kind=pmp.GenKind.Mixed,
+                                                       weights=pmp.WeightDist.uniform(0.5, 1.5), seed=13),
+                                           0.005, 0.10),
+    "ragged": _ragged_problem,
+    # every stream on one link: a single row of n entries
+    "one_link": lambda: pmp.build_problem([pmp.Stream(j, pmp.StreamKind.Log, "", 1.0 + 0.001 * j, [0])
+                                           for j in range(5000)], [3.0]),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(SHAPE_CASES))
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_skewed_and_ragged_shapes_match_oracle(shape, blocks, restatement, oracle_mod, monkeypatch):
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", str(blocks))
+    p = SHAPE_CASES[shape]()
+    cfg = (pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0, max_iters=20000) if shape == "congested"
+           else pmp.SolverConfig(eps_abs=1e-5, rho0=1.0, max_iters=20000))
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert ref.error is None
+    assert sol.iterations == ref.iterations and int(sol.status) == ref.status
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
+    assert abs(sol.objective - ref.objective) <= RTOL * abs(ref.objective)
