@@ -166,11 +166,6 @@ struct BlockArgs {
   long long nv, nu;
   int index;           // block number b
   int first;           // b == 0
-  // stream units of k_stream_pass (kK1Units): consecutive streams whose
-  // routes, cut into segments of <= sseg entries, fill <= 32 lanes
-  const int* su;       // nsu+1: first stream of each unit, relative to s0
-  long long nsu;
-  int sseg;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -400,94 +395,6 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
   }
 }
 
-// Stream units: the warp takes a unit of consecutive streams whose routes,
-// cut into segments of <= sseg entries (near-equal split), fill at most 32
-// lanes; one lane per segment, so a lane's gather chain is short and every
-// lane has its whole segment in flight.  The lane -> (stream, segment) map
-// is rebuilt in registers from col_ptr (a scan of the per-stream segment
-// counts and a shuffle binary search); a segmented scan over the lanes
-// leaves zeta's gather sum at the stream's last segment, whose lane runs the
-// prox and the A update.
-template <class G>
-__device__ __forceinline__ void stream_units_body(const IterArgs& a, const BlockArgs& bk, G g,
-                                                  double rho, bool trace_it, int* sidx,
-                                                  double& p_tda2, double& p_obj) {
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_last = policy_evict_last();
-  const double alpha = a.alpha;
-  const int S = bk.sseg;
-  for (long long u = (long long)blockIdx.x * kWarps + wib; u < bk.nsu;
-       u += (long long)gridDim.x * kWarps) {
-    const long long j0 = bk.s0 + __ldg(bk.su + u);
-    const int nstr = static_cast<int>(bk.s0 + __ldg(bk.su + u + 1) - j0);  // <= 32
-    const bool own = lane < nstr;  // lane owns stream j0 + lane's state
-    const long long js = j0 + (own ? lane : 0);
-    const int b = __ldg(a.col_ptr + js);
-    const int e = own ? __ldg(a.col_ptr + js + 1) : b;
-    const int tau = e - b;
-    const int nseg = own ? max(1, (tau + S - 1) / S) : 0;
-    double A = 0.0, w = 0.0;
-    int kd = 0;
-    if (own) {  // needed only after the gather: issue early
-      A = ld_stream_f64(a.A_in + js, pol_first);
-      w = __ldg(a.w + js);
-      kd = __ldg(a.kind + js);
-    }
-    int cs = nseg;  // inclusive scan of the segment counts
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int t = __shfl_up_sync(kFull, cs, d);
-      if (lane >= d) cs += t;
-    }
-    const int total = __shfl_sync(kFull, cs, 31);
-    int si = 0;  // my segment's stream: #streams whose segments end at or before lane
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1)
-      if (__shfl_sync(kFull, cs, si + step - 1) <= lane) si += step;
-    si = min(si, 31);
-    const bool valid = lane < total;
-    const int prev_cs = __shfl_sync(kFull, cs, max(si - 1, 0));
-    const int k = lane - (si > 0 ? prev_cs : 0);
-    const int sb = __shfl_sync(kFull, b, si);
-    const int st = __shfl_sync(kFull, tau, si);
-    const int sn = __shfl_sync(kFull, nseg, si);
-    const int span_beg = __shfl_sync(kFull, b, 0);
-    const int span_end = __shfl_sync(kFull, e, max(nstr - 1, 0));
-    int vb = span_end, ve = span_end;
-    if (valid) {
-      vb = sb + static_cast<int>((static_cast<long long>(k) * st) / sn);
-      ve = sb + static_cast<int>((static_cast<long long>(k + 1) * st) / sn);
-    }
-    double sum = warp_segments_sum(a.row_idx, span_beg, span_end, vb, ve, sidx, lane, g, pol_first);
-    const int row = valid ? si : -1 - lane;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal streams
-      const double t = __shfl_up_sync(kFull, sum, d);
-      const int tr = __shfl_up_sync(kFull, row, d);
-      if (lane >= d && tr == row) sum += t;
-    }
-    const int next_row = __shfl_down_sync(kFull, row, 1);
-    const double Ai = __shfl_sync(kFull, A, si);
-    const double wi = __shfl_sync(kFull, w, si);
-    const int kdi = __shfl_sync(kFull, kd, si);
-    if (!valid || (lane != 31 && next_row == row)) continue;  // not the stream's last segment
-    const long long j = j0 + si;
-    const double zeta = static_cast<double>(st) * Ai - sum;
-    const double x = (kdi == NUMPMP_KIND_LOG) ? prox_log(zeta, wi, rho, st)
-                                              : prox_linear_nonneg(zeta, wi, rho, st);
-    const double An = alpha * x + (1.0 - alpha) * Ai;
-    const double dA = An - Ai;
-    st_hint_f64(a.x + j, x, pol_last);
-    st_hint_f64(a.A_out + j, An, pol_first);
-    p_tda2 += static_cast<double>(st) * dA * dA;
-    if (trace_it) p_obj += (kdi == NUMPMP_KIND_LOG) ? wi * log(x) : wi * x;
-  }
-}
-
-// kMode 0: 32-stream tiles, one lane per stream (stream_pass_body);
-// kMode 1: stream units (stream_units_body).
-template <int kMode>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
   __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
@@ -498,10 +405,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   int* sb = sidx[threadIdx.x >> 5];
   const int sel = a.ctrl->v_sel;
   const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  if (kMode == 0)
-    stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
-  else
-    stream_units_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
+  stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 

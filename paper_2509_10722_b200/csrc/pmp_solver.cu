@@ -147,9 +147,6 @@ struct ColBlock {
   int* uptr = nullptr;        // nu+1: first segment of each warp unit
   int64_t nu = 0;
   int seg = 0;                // max entries per segment
-  int* su = nullptr;          // nsu+1: stream units of k_stream_pass<1> (first stream, relative to s0)
-  int64_t nsu = 0;
-  int sseg = 0;               // max route entries per stream segment
 };
 
 }  // namespace
@@ -161,7 +158,6 @@ struct numpmp_gpu {
   cudaEvent_t pipe_ev[2 * kMaxBlocks + 2] = {};
   bool split_epilogue = true;      // NUMPMP_SPLIT_EPILOGUE=0: epilogue fused into the last link pass
   bool pipeline = true;            // NUMPMP_PIPELINE=0: serial graph (K1(b+1) no longer overlaps K2(b))
-  bool k1_units = true;            // NUMPMP_K1_UNITS=0: stream pass in 32-stream tiles
   std::string err;
   numpmp_config cfg{};
   int64_t m = 0, n = 0, nnz = 0;
@@ -356,9 +352,6 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.nu = cb.nu;
   k.index = b;
   k.first = b == 0;
-  k.su = cb.su;
-  k.nsu = cb.nsu;
-  k.sseg = cb.sseg;
   return k;
 }
 
@@ -368,13 +361,6 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
 // followed by the NCCL all-reduce of the partial loads and the replicated
 // epilogue (sharded).  ev (nullable): events[0..launches] recorded around
 // every launch; ev[0] is skipped when record_first is false.
-void launch_stream_pass(numpmp_gpu* h, const IterArgs& a, const BlockArgs& bk, cudaStream_t st) {
-  if (h->k1_units)
-    k_stream_pass<1><<<h->grid1, kThreads, 0, st>>>(a, bk);
-  else
-    k_stream_pass<0><<<h->grid1, kThreads, 0, st>>>(a, bk);
-}
-
 void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, bool record_first) {
   IterArgs a = make_args(h, parity, mode);
   int e = 0;
@@ -398,7 +384,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
   }
   for (int b = 0; b < nb; ++b) {
     const BlockArgs bk = block_args(h, b);
-    launch_stream_pass(h, a, bk, h->stream);
+    k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
     mark(1);
     if (b + 1 < nb || (h->split_epilogue && !h->sharded))
       k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
@@ -445,7 +431,7 @@ void enqueue_iteration_pipelined(numpmp_gpu* h, int parity, int mode) {
   for (int b = 0; b < nb; ++b) {
     const BlockArgs bk = block_args(h, b);
     if (b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    launch_stream_pass(h, a, bk, h->stream2);
+    k_stream_pass<<<h->grid1, kThreads, 0, h->stream2>>>(a, bk);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev_k1[b], h->stream2));
     CK(cudaStreamWaitEvent(h->stream, ev_k1[b], 0));
@@ -728,7 +714,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   for (cudaEvent_t& e : h->pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* env = std::getenv("NUMPMP_SPLIT_EPILOGUE")) h->split_epilogue = std::atoi(env) != 0;
   if (const char* env = std::getenv("NUMPMP_PIPELINE")) h->pipeline = std::atoi(env) != 0;
-  if (const char* env = std::getenv("NUMPMP_K1_UNITS")) h->k1_units = std::atoi(env) != 0;
   // L2 set-aside for the evict_last lines (x of the live column blocks, v):
   // 32 MB measured best at config C (profiles/r1_l2_sweep.txt);
   // NUMPMP_L2_PERSIST_MB overrides (0 = leave the device limit alone).
@@ -841,7 +826,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
   int occ3 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
@@ -850,41 +835,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
     max_nu = std::max(max_nu, cb.nu);
   }
-  // stream units (k_stream_pass<1>): route segments of <= sseg entries,
-  // consecutive streams packed greedily into units of <= 32 segments
-  int64_t max_nsu = 0;
-  {
-    int base_seg = 16;
-    if (const char* env = std::getenv("NUMPMP_K1_SEG")) base_seg = std::max(1, std::atoi(env));
-    for (ColBlock& cb : h->blocks) {
-      int64_t maxt = 0;
-      for (int64_t j = cb.s0; j < cb.s1; ++j)
-        maxt = std::max<int64_t>(maxt, pv->stream_offsets[j + 1] - pv->stream_offsets[j]);
-      cb.sseg = static_cast<int>(std::max<int64_t>(base_seg, (maxt + 31) / 32));
-      std::vector<int> su;
-      su.reserve(static_cast<size_t>((cb.s1 - cb.s0) / 16 + 2));
-      su.push_back(0);
-      int used = 0, nstr = 0;
-      for (int64_t j = cb.s0; j < cb.s1; ++j) {
-        const int64_t t = pv->stream_offsets[j + 1] - pv->stream_offsets[j];
-        const int ns = static_cast<int>(std::max<int64_t>(1, (t + cb.sseg - 1) / cb.sseg));
-        if (used + ns > 32 || nstr == 32) {
-          su.push_back(static_cast<int>(j - cb.s0));
-          used = 0;
-          nstr = 0;
-        }
-        used += ns;
-        ++nstr;
-      }
-      su.push_back(static_cast<int>(cb.s1 - cb.s0));
-      cb.nsu = static_cast<int64_t>(su.size()) - 1;
-      cb.su = dalloc<int>(su.size(), b, h->stream);
-      CK(cudaMemcpyAsync(cb.su, su.data(), sizeof(int) * su.size(), cudaMemcpyHostToDevice, h->stream));
-      CK(cudaStreamSynchronize(h->stream));
-      max_nsu = std::max(max_nsu, cb.nsu);
-    }
-  }
-  const long long tiles1 = h->k1_units ? max_nsu : (max_bs + 31) / 32, tiles2 = max_nu;
+  const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
   h->grid1 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ1, 1))));
   h->grid2 = static_cast<int>(std::max(
@@ -1788,7 +1739,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   for (ColBlock& cb : h->blocks)
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
                     static_cast<void*>(cb.uptr), static_cast<void*>(cb.vptr),
-                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.su)})
+                    static_cast<void*>(cb.vrow)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {
