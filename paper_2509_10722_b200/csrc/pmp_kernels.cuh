@@ -61,13 +61,6 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
 constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
-#ifndef NUMPMP_VEC_IDX
-#define NUMPMP_VEC_IDX 1
-#endif
-static_assert(kUnroll % 4 == 0 || !NUMPMP_VEC_IDX, "vector index loads need kUnroll % 4 == 0");
-// staging rows are padded so the vector index loads of the last batch stay
-// inside the warp's buffer
-constexpr int kStagePad = NUMPMP_VEC_IDX ? kUnroll + 4 : 0;
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kMaxBlocks = 16;                 // max column blocks
 constexpr unsigned kFull = 0xffffffffu;
@@ -286,34 +279,9 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
     // fewer than min(kUnroll, remaining) gathers in flight (the passes are
     // bound by outstanding L1->L2 requests, not by instructions).
     for (int k = lo; k < hi; k += kUnroll) {
-      int ii[kUnroll];
-#if NUMPMP_VEC_IDX
-      // The batch's indices with 16-byte shared loads (kUnroll/4 + 1 instead
-      // of kUnroll 4-byte loads: fewer MIO instructions per gather), then a
-      // register select on the misalignment.
-      {
-        const int r0 = k - cb;
-        const int q = r0 >> 2, off = r0 & 3;
-        int w[kUnroll + 4];
-#pragma unroll
-        for (int t = 0; t < kUnroll / 4 + 1; ++t) {
-          const int4 v4 = reinterpret_cast<const int4*>(sidx)[q + t];
-          w[4 * t] = v4.x;
-          w[4 * t + 1] = v4.y;
-          w[4 * t + 2] = v4.z;
-          w[4 * t + 3] = v4.w;
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          ii[u] = off == 0 ? w[u] : (off == 1 ? w[u + 1] : (off == 2 ? w[u + 2] : w[u + 3]));
-      }
-#else
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) ii[u] = (k + u < hi) ? sidx[k + u - cb] : 0;
-#endif
       double vv[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + u < hi) ? g(ii[u]) : 0.0;
+      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + u < hi) ? g(sidx[k + u - cb]) : 0.0;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
         if (k + u < hi) acc += vv[u];
@@ -428,7 +396,7 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts + kStagePad];
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
   const long long k = a.ctrl->run_k + 1;
@@ -601,7 +569,7 @@ template <int kPhase>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts + kStagePad];
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   __shared__ bool s_last;
   if (a.mode != MODE_AUX && kernel_should_exit(a.ctrl)) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
