@@ -11,10 +11,7 @@ build() {  # name, extra nvcc flags...
     paper_2509_10722_b200/csrc/pmp_solver.cu paper_2509_10722_b200/csrc/host_gen.cpp paper_2509_10722_b200/csrc/host_io.cpp -ldl -cudart static &
 }
 build base
-build u4_minb6 -DNUMPMP_GATHER_UNROLL=4 -DNUMPMP_MIN_BLOCKS=6
-build u4_minb8 -DNUMPMP_GATHER_UNROLL=4 -DNUMPMP_MIN_BLOCKS=8
-build u2_minb8 -DNUMPMP_GATHER_UNROLL=2 -DNUMPMP_MIN_BLOCKS=8
-build u8_minb5 -DNUMPMP_GATHER_UNROLL=8 -DNUMPMP_MIN_BLOCKS=5
-build w4_u4_minb12 -DNUMPMP_WARPS=4 -DNUMPMP_GATHER_UNROLL=4 -DNUMPMP_MIN_BLOCKS=12
+build unroll4 -DNUMPMP_GATHER_UNROLL=4
+build unroll12 -DNUMPMP_GATHER_UNROLL=12
 wait
 ls -la build/variants
