@@ -345,10 +345,20 @@ __device__ __forceinline__ bool kernel_should_exit(const Ctrl* ctrl) {
 // the iteration's first stream pass.  Exits at entry otherwise.
 __global__ void __launch_bounds__(kThreads) k_refresh_v(IterArgs a) {
   if (a.ctrl->rho_changed == 0) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->v_sel = 0;
   const double rho = a.ctrl->rho;
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < a.m;
        l += (long long)gridDim.x * blockDim.x)
     a.v[l] = a.B_in[l] + a.pr_in[l] / rho;
+}
+
+// v = B + price / rho unconditionally (outside the loop), v_sel = 0.
+__global__ void __launch_bounds__(256) k_set_v(IterArgs a) {
+  const double rho = a.ctrl->rho;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < a.m;
+       l += (long long)gridDim.x * blockDim.x)
+    a.v[l] = a.B_in[l] + a.pr_in[l] / rho;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->v_sel = 0;
 }
 
 // ------------------------------------------------------------ K1: streams
@@ -414,7 +424,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
 // (110-126), z update split into B / zs / Q (388-399), price (401-405).
 __device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, double L, int d,
                                               double rho, double (&part)[4], uint64_t pol,
-                                              uint64_t pol_last) {
+                                              uint64_t pol_last, double* Bn_out = nullptr,
+                                              double* prn_out = nullptr) {
   const double alpha = a.alpha;
   const double c = __ldg(a.cap + r);
   const double pr = ld_stream_f64(a.pr_in + r, pol);
@@ -442,6 +453,10 @@ __device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, 
   a.pr_out[r] = prn;
   const double vn = Bn + prn / rho;
   st_hint_f64(a.v + r, vn, pol_last);
+  if (Bn_out) {
+    *Bn_out = Bn;
+    *prn_out = prn;
+  }
   if (a.v_alt[0] != nullptr && a.mode == MODE_RUN && (a.ctrl->run_k + 1) % a.rho_interval == 0) {
     // the rhos finalize_iteration may switch to, computed as it does
     st_hint_f64(a.v_alt[0] + r, Bn + prn / (rho * a.gamma), pol_last);

@@ -23,10 +23,9 @@
 //                        rank takes the same termination / rho decision --
 //                        and runs finalize_iteration.
 //
-// After a rho change v must be rebuilt from B and price, which are current
-// only on the owners: k_p2p_refresh_v (owned links, scattered to every
-// rank) + k_p2p_wait<2> run first in every iteration and exit at entry
-// unless rho_changed.  Traffic per rank and iteration: 8 (world-1)/world
+// On rho-update iterations the owner also stores v for both candidate rhos
+// (rho*gamma, rho/gamma) into every rank; finalize_iteration selects one
+// (Ctrl::v_sel), so nothing rebuilds v inside the loop.  Traffic per rank and iteration: 8 (world-1)/world
 // bytes per link in each direction, the same as a ring all-reduce, but the
 // epilogue work is divided by world and no NCCL kernel sits in the loop.
 //
@@ -41,7 +40,7 @@
 // i this rank has completed, identical on all ranks because every rank runs
 // the same sequence: target = world * (done_cnt[i] + 1).
 //   flags[0] loads stored / aux push, flags[1] epilogue done / aux result,
-//   flags[2] v refreshed, flags[3] aux buffers free.
+//   flags[3] aux buffers free (flags[2] unused).
 #pragma once
 
 #include "pmp_kernels.cuh"
@@ -74,32 +73,11 @@ __device__ __forceinline__ void p2p_signal_all(const P2PArgs& p, int which) {
 }
 
 // ---------------------------------------------------------------- iteration
-// kCheck: 0 = always wait, 1 = only if rho_changed (the v refresh barrier).
-template <int kWhich, int kOnlyIfRhoChanged>
+template <int kWhich>
 __global__ void k_p2p_wait(IterArgs a) {
   if (threadIdx.x != 0) return;
   if (kernel_should_exit(a.ctrl)) return;
-  if (kOnlyIfRhoChanged && a.ctrl->rho_changed == 0) return;
   p2p_wait_counter(a.p2p, kWhich);
-}
-
-__global__ void __launch_bounds__(kThreads) k_p2p_refresh_v(IterArgs a) {
-  __shared__ bool s_last;
-  if (kernel_should_exit(a.ctrl) || a.ctrl->rho_changed == 0) return;
-  const double rho = a.ctrl->rho;
-  const P2PArgs& p = a.p2p;
-  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
-       l += (long long)gridDim.x * blockDim.x) {
-    const double v = a.B_in[l] + a.pr_in[l] / rho;
-    for (int q = 0; q < p.world; ++q) ld_ptr(p.v_peer + q)[l] = v;
-  }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket3, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
-  a.ctrl->ticket3 = 0;
-  p2p_signal_all(p, 2);
 }
 
 __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
@@ -111,13 +89,25 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
   const uint64_t pol_last = policy_evict_last();
   double part[4] = {0.0, 0.0, 0.0, 0.0};
   const double* slots = ld_ptr(p.slots_peer + p.rank);
+  // rho-update iteration: v for both candidate rhos too (finalize picks one)
+  const bool cand = a.mode == MODE_RUN && (a.ctrl->run_k + 1) % a.rho_interval == 0;
   for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
        l += (long long)gridDim.x * blockDim.x) {
     double L = 0.0;
     for (int q = 0; q < p.world; ++q) L += __ldcg(slots + q * p.mo + (l - p.l0));
-    const double v = link_epilogue(a, l, L, __ldg(a.deg + l), rho, part, pol_first, pol_last);
-    for (int q = 0; q < p.world; ++q)
-      if (q != p.rank) ld_ptr(p.v_peer + q)[l] = v;
+    double Bn, prn;
+    const double v = link_epilogue(a, l, L, __ldg(a.deg + l), rho, part, pol_first, pol_last, &Bn, &prn);
+    const double vu = cand ? Bn + prn / (rho * a.gamma) : 0.0;
+    const double vd = cand ? Bn + prn / (rho / a.gamma) : 0.0;
+    for (int q = 0; q < p.world; ++q) {
+      if (q == p.rank) continue;  // local copies written by link_epilogue
+      double* vq = ld_ptr(p.v_peer + q);
+      vq[l] = v;
+      if (cand) {
+        vq[a.m + l] = vu;
+        vq[2 * a.m + l] = vd;
+      }
+    }
   }
   block_sum_store<4>(part, p.ep_part + 4 * blockIdx.x);
   __threadfence_system();

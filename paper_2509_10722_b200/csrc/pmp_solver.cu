@@ -234,7 +234,7 @@ struct numpmp_gpu {
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
   int launches_per_iteration() const {
-    return p2p ? 2 * nb() + 5 : 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
+    return p2p ? 2 * nb() + 3 : 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
   }
   std::vector<int> launch_side;  // per launch of an iteration: 1 stream side, 2 link side
 };
@@ -262,9 +262,9 @@ const char* validate_config(const numpmp_config* c) {
   return nullptr;
 }
 
-// Exchange region layout: [v: m][slots: world*mo][xs: world*8] doubles,
-// then [flags: 4] u64.
-size_t xr_slots_off(const numpmp_gpu* h) { return 8 * static_cast<size_t>(h->m); }
+// Exchange region layout: [v: m][v_alt: 2m][slots: world*mo][xs: world*8]
+// doubles, then [flags: 4] u64.
+size_t xr_slots_off(const numpmp_gpu* h) { return 24 * static_cast<size_t>(h->m); }
 size_t xr_xs_off(const numpmp_gpu* h) {
   return xr_slots_off(h) + 8 * static_cast<size_t>(h->world) * static_cast<size_t>(h->mo);
 }
@@ -322,8 +322,8 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   a.Q_in = h->Q[i];
   a.Q_out = h->Q[o];
   a.v = h->v;
-  a.v_alt[0] = h->p2p ? nullptr : h->v_alt[0];
-  a.v_alt[1] = h->p2p ? nullptr : h->v_alt[1];
+  a.v_alt[0] = h->v_alt[0];
+  a.v_alt[1] = h->v_alt[1];
   a.k1_part = h->k1_part;
   a.k2_part = h->k2_part;
   a.grid1 = h->grid1;
@@ -361,7 +361,17 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
 // followed by the NCCL all-reduce of the partial loads and the replicated
 // epilogue (sharded).  ev (nullable): events[0..launches] recorded around
 // every launch; ev[0] is skipped when record_first is false.
-void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, bool record_first) {
+// One PMP iteration: for each column block b the stream pass K1(b) and the
+// link pass K2(b), then the tail: the streaming link epilogue + finalize
+// (one device), the NCCL all-reduce + replicated epilogue, or the
+// peer-memory wait / owner epilogue / finalize (pmp_p2p.cuh).
+// pipelined: the stream passes run on a side stream, so K1(b+1) fills
+// K2(b)'s tail; K1(b+2) waits for K2(b) (at most two x blocks live in L2).
+// Launch order, work split and summation order are those of the serial
+// form, so results are bit-identical.  ev (serial form only, nullable):
+// events[0..launches] around every launch; ev[0] skipped unless record_first.
+void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, bool record_first,
+                       bool pipelined = false) {
   IterArgs a = make_args(h, parity, mode);
   int e = 0;
   std::vector<int> side;
@@ -371,22 +381,27 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     ++e;
     side.push_back(s);
   };
-  if (record_first) {
-    if (ev) CK(cudaEventRecordWithFlags(ev[0], h->stream, cudaEventRecordExternal));
-  }
+  if (record_first && ev) CK(cudaEventRecordWithFlags(ev[0], h->stream, cudaEventRecordExternal));
   ++e;
   const int nb = h->nb();
-  if (h->p2p) {
-    k_p2p_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(a);
-    mark(1);
-    k_p2p_wait<2, 1><<<1, 32, 0, h->stream>>>(a);
-    mark(1);
+  cudaEvent_t* ev_k1 = h->pipe_ev;               // [nb]: K1(b) done
+  cudaEvent_t* ev_k2 = h->pipe_ev + kMaxBlocks;  // [nb]: K2(b) done
+  if (pipelined) {
+    CK(cudaEventRecord(h->pipe_ev[2 * kMaxBlocks], h->stream));
+    CK(cudaStreamWaitEvent(h->stream2, h->pipe_ev[2 * kMaxBlocks], 0));
   }
+  const bool acc_last = h->split_epilogue && !h->sharded;
   for (int b = 0; b < nb; ++b) {
     const BlockArgs bk = block_args(h, b);
-    k_stream_pass<<<h->grid1, kThreads, 0, h->stream>>>(a, bk);
+    cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
+    if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
+    k_stream_pass<<<h->grid1, kThreads, 0, s1>>>(a, bk);
     mark(1);
-    if (b + 1 < nb || (h->split_epilogue && !h->sharded))
+    if (pipelined) {
+      CK(cudaEventRecord(ev_k1[b], h->stream2));
+      CK(cudaStreamWaitEvent(h->stream, ev_k1[b], 0));
+    }
+    if (b + 1 < nb || acc_last)
       k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else if (h->p2p)
       k_link_pass<LP_P2P><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
@@ -395,9 +410,10 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     else
       k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     mark(2);
+    if (pipelined) CK(cudaEventRecord(ev_k2[b], h->stream));
   }
   if (h->p2p) {
-    k_p2p_wait<0, 0><<<1, 32, 0, h->stream>>>(a);
+    k_p2p_wait<0><<<1, 32, 0, h->stream>>>(a);
     mark(2);
     k_p2p_epilogue<<<h->grid3, kThreads, 0, h->stream>>>(a);
     mark(2);
@@ -408,44 +424,11 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
                  h->stream));
     k_link_epilogue<0><<<h->grid3, kThreads, 0, h->stream>>>(a);
     mark(2);
-  } else if (h->split_epilogue) {
+  } else if (acc_last) {
     k_link_epilogue<1><<<h->grid3, kThreads, 0, h->stream>>>(a);
     mark(2);
   }
   h->launch_side = side;
-}
-
-// The same iteration with the stream passes on a side stream: K1(b+1) may
-// run while K2(b) drains (filling its tail), K1(b+2) waits for K2(b) so at
-// most two x blocks are live in L2.  Launch order, work split and summation
-// order are unchanged, so results are bit-identical to the serial graph.
-// Single device only; used for graphs without per-launch events.
-void enqueue_iteration_pipelined(numpmp_gpu* h, int parity, int mode) {
-  IterArgs a = make_args(h, parity, mode);
-  const int nb = h->nb();
-  cudaEvent_t* ev_k1 = h->pipe_ev;            // [nb]: K1(b) done
-  cudaEvent_t* ev_k2 = h->pipe_ev + kMaxBlocks;  // [nb]: K2(b) done
-  cudaEvent_t ev_start = h->pipe_ev[2 * kMaxBlocks];
-  CK(cudaEventRecord(ev_start, h->stream));
-  CK(cudaStreamWaitEvent(h->stream2, ev_start, 0));
-  for (int b = 0; b < nb; ++b) {
-    const BlockArgs bk = block_args(h, b);
-    if (b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    k_stream_pass<<<h->grid1, kThreads, 0, h->stream2>>>(a, bk);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ev_k1[b], h->stream2));
-    CK(cudaStreamWaitEvent(h->stream, ev_k1[b], 0));
-    if (b + 1 < nb || h->split_epilogue)
-      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
-    else
-      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ev_k2[b], h->stream));
-  }
-  if (h->split_epilogue) {
-    k_link_epilogue<1><<<h->grid3, kThreads, 0, h->stream>>>(a);
-    CK(cudaGetLastError());
-  }
 }
 
 cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
@@ -455,12 +438,9 @@ cudaGraphExec_t build_graph(numpmp_gpu* h, int parity, int ev_set) {
   CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   try {
     for (int i = 0; i < kBatchIters; ++i) {
-      if (h->pipeline && ev_set < 0 && !h->sharded)
-        enqueue_iteration_pipelined(h, parity ^ (i & 1), MODE_RUN);
-      else
-        enqueue_iteration(h, parity ^ (i & 1), MODE_RUN,
-                          ev_set >= 0 ? &h->prof_ev[set_base + static_cast<size_t>(i * lpi)] : nullptr,
-                          i == 0);
+      enqueue_iteration(h, parity ^ (i & 1), MODE_RUN,
+                        ev_set >= 0 ? &h->prof_ev[set_base + static_cast<size_t>(i * lpi)] : nullptr,
+                        i == 0, h->pipeline && ev_set < 0);
     }
   } catch (...) {
     cudaStreamEndCapture(h->stream, &g);
@@ -492,7 +472,7 @@ Ctrl read_ctrl(numpmp_gpu* h) {
 // ------------------------------------------ peer-memory collectives (aux)
 // Outside the iteration loop (pmp_p2p.cuh): every call is collective over
 // the ranks, which run the same sequence.  They use v as the result buffer,
-// so v is marked stale afterwards (rebuilt by k_p2p_refresh_v).
+// so v is rebuilt afterwards (p2p_mark_v_stale).
 void p2p_barrier(numpmp_gpu* h, int which) {
   const P2PArgs p = p2p_args(h);
   k_p2p_aux_signal<<<1, 32, 0, h->stream>>>(p, which);
@@ -500,9 +480,12 @@ void p2p_barrier(numpmp_gpu* h, int which) {
   k_p2p_aux_wait<<<1, 32, 0, h->stream>>>(p, which);
   CK(cudaGetLastError());
 }
+// v was used as a result buffer: rebuild it from B and price (current on
+// every rank outside the loop: after set_cold / set_warm, or after
+// p2p_sync_link_state) with the next iteration's rho.
 void p2p_mark_v_stale(numpmp_gpu* h) {
-  static const int one = 1;
-  CK(cudaMemcpyAsync(&h->ctrl->rho_changed, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  k_set_v<<<grid_for(h->m), 256, 0, h->stream>>>(make_args(h, h->cur, MODE_AUX));
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
 }
 // dst[0:m) = sum over ranks of src[0:m) (rank order); src may alias dst.
@@ -1099,7 +1082,11 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
       CK(cudaMalloc(&h->xregion, h->xregion_bytes));
       CK(cudaMemsetAsync(h->xregion, 0, h->xregion_bytes, h->stream));
       cudaFreeAsync(h->v, h->stream);
+      cudaFreeAsync(h->v_alt[0], h->stream);
+      cudaFreeAsync(h->v_alt[1], h->stream);
       h->v = static_cast<double*>(h->xregion);
+      h->v_alt[0] = h->v + h->m;
+      h->v_alt[1] = h->v + 2 * h->m;
       int64_t* b = &h->dev_bytes;
       h->done_cnt = dalloc<unsigned long long>(4, b, h->stream);
       CK(cudaMemsetAsync(h->done_cnt, 0, 4 * sizeof(unsigned long long), h->stream));
@@ -1716,7 +1703,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   for (void* base : h->peer_bases) cudaIpcCloseMemHandle(base);
   if (h->xregion) {
     cudaFree(h->xregion);
-    h->v = nullptr;  // lived in the exchange region
+    h->v = h->v_alt[0] = h->v_alt[1] = nullptr;  // lived in the exchange region
   }
   std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
