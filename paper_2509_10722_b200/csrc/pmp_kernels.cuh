@@ -377,8 +377,10 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
        tile += (long long)gridDim.x * kWarps) {
     const long long j = bk.s0 + tile * 32 + lane;
     const bool valid = j < bk.s1;
+    // two independent offset loads (no select on a loaded value, so the
+    // second load is not held back by the first)
     const int beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
-    const int end = valid ? __ldg(a.col_ptr + j + 1) : beg;
+    const int end = __ldg(a.col_ptr + (valid ? j + 1 : bk.s1));
     double A = 0.0, w = 0.0;
     int kd = 0;
     if (valid) {  // independent of the gather: issue early
@@ -390,6 +392,10 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
     const int span_end = __shfl_sync(kFull, end, 31);
     const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
                                          pol_first);
+    // keep the kind test (and with it the wait for the kind / weight loads)
+    // after the gather loop: the compiler otherwise hoists it and the warp
+    // stalls on those loads before issuing any gather
+    asm volatile("" : "+r"(kd), "+d"(w) : : "memory");
     if (valid) {
       const int tau = end - beg;
       const double zeta = static_cast<double>(tau) * A - sum;
