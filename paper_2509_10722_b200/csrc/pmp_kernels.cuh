@@ -598,14 +598,28 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   const uint64_t pol_last = policy_evict_last();
   const double rho = (kPhase == LP_FUSED) ? a.ctrl->rho : 0.0;
   double part[4] = {0.0, 0.0, 0.0, 0.0};
-  for (long long u = (long long)blockIdx.x * kWarps + wib; u < bk.nu;
-       u += (long long)gridDim.x * kWarps) {
-    const int v0 = __ldg(bk.uptr + u), v1 = __ldg(bk.uptr + u + 1);
+  const long long ustride = (long long)gridDim.x * kWarps;
+  long long u = (long long)blockIdx.x * kWarps + wib;
+  // this unit's segment range, loaded one unit ahead (the uptr -> vptr chain
+  // would otherwise put two dependent loads in front of every unit)
+  int v0 = 0, v1 = 0;
+  if (u < bk.nu) {
+    v0 = __ldg(bk.uptr + u);
+    v1 = __ldg(bk.uptr + u + 1);
+  }
+  for (; u < bk.nu; u += ustride) {
     const int v = v0 + lane;
     const bool valid = v < v1;
+    // independent loads, no select on a loaded value (it would hold the
+    // next load back until the first one returns)
     const int vb = __ldg(bk.vptr + (valid ? v : v1));
-    const int ve = valid ? __ldg(bk.vptr + v + 1) : vb;
-    const int row = valid ? __ldg(bk.vrow + v) : -1 - lane;
+    const int ve = __ldg(bk.vptr + (valid ? v + 1 : v1));
+    int row = -1 - lane;
+    if (valid) row = __ldg(bk.vrow + v);
+    if (u + ustride < bk.nu) {
+      v0 = __ldg(bk.uptr + u + ustride);
+      v1 = __ldg(bk.uptr + u + ustride + 1);
+    }
     const int span_beg = __shfl_sync(kFull, vb, 0);
     const int span_end = __shfl_sync(kFull, ve, 31);
     double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
