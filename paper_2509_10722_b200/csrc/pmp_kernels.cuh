@@ -292,59 +292,6 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
   return acc;
 }
 
-// warp_segments_sum for a warp that walks a sequence of spans (the stream
-// pass's tiles): on entry buf holds the first staged round of this span; the
-// round after the span's last one is the FIRST round of the next span
-// [next_beg, next_end) (next_beg < 0: none), so the next item's index load
-// overlaps this item's gathers instead of starting after them.
-template <class G>
-__device__ __forceinline__ double warp_segments_sum_chain(const int* __restrict__ idx, int span_beg,
-                                                          int span_end, int seg_beg, int seg_end,
-                                                          int* __restrict__ sidx, int lane, G g,
-                                                          uint64_t pol_stream,
-                                                          int4 (&buf)[kStageInts / 128], int next_beg,
-                                                          int next_end) {
-  constexpr int NV = kStageInts / 128;
-  double acc = 0.0;
-  int cb = span_beg & ~3;
-  while (cb < span_end) {
-    const int c1 = min(cb + kStageInts, span_end);
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int o = 4 * (lane + 32 * i);
-      if (cb + o < c1) *reinterpret_cast<int4*>(sidx + o) = buf[i];
-    }
-    __syncwarp();
-    const int nb = cb + kStageInts;
-    if (nb < span_end) {
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int gp = nb + 4 * (lane + 32 * i);
-        if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
-      }
-    } else if (next_beg >= 0) {  // this span is done after this round: start the next one
-      const int nc = next_beg & ~3;
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int gp = nc + 4 * (lane + 32 * i);
-        if (gp < next_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
-      }
-    }
-    const int lo = max(seg_beg, cb), hi = min(seg_end, c1);
-    for (int k = lo; k < hi; k += kUnroll) {
-      double vv[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + u < hi) ? g(sidx[k + u - cb]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (k + u < hi) acc += vv[u];
-    }
-    __syncwarp();
-    cb = nb;
-  }
-  return acc;
-}
-
 // Fixed-order block reduction of NV partials; thread 0 writes out[0..NV).
 template <int NV>
 __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* out) {
@@ -421,42 +368,19 @@ template <class G>
 __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockArgs& bk, G g,
                                                  double rho, bool trace_it, int* sidx,
                                                  double& p_tda2, double& p_obj) {
-  constexpr int NV = kStageInts / 128;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
   const long long ntiles = (bk.s1 - bk.s0 + 31) / 32;
-  const long long tstride = (long long)gridDim.x * kWarps;
   const double alpha = a.alpha;
-  long long tile = (long long)blockIdx.x * kWarps + wib;
-  if (tile >= ntiles) return;
-  // Software pipeline over the warp's tiles: the next tile's offsets are
-  // loaded at the start of this one, and its first index round is loaded
-  // (into buf) while this tile gathers.
-  auto offsets = [&](long long t, int& beg, int& end) {  // two independent loads
-    const long long j = bk.s0 + t * 32 + lane;
-    const bool valid = j < bk.s1;
-    beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
-    end = __ldg(a.col_ptr + (valid ? j + 1 : bk.s1));
-  };
-  int beg, end;
-  offsets(tile, beg, end);
-  int4 buf[NV];
-  {
-    const int sb = __shfl_sync(kFull, beg, 0), se = __shfl_sync(kFull, end, 31);
-    const int cb = sb & ~3;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int gp = cb + 4 * (lane + 32 * i);
-      if (gp < se) buf[i] = ld_stream_int4(a.row_idx + gp, pol_first);
-    }
-  }
-  for (; tile < ntiles; tile += tstride) {
+  for (long long tile = (long long)blockIdx.x * kWarps + wib; tile < ntiles;
+       tile += (long long)gridDim.x * kWarps) {
     const long long j = bk.s0 + tile * 32 + lane;
     const bool valid = j < bk.s1;
-    const bool has_next = tile + tstride < ntiles;
-    int nbeg = -1, nend = -1;
-    if (has_next) offsets(tile + tstride, nbeg, nend);
+    // two independent offset loads (no select on a loaded value, so the
+    // second load is not held back by the first)
+    const int beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
+    const int end = __ldg(a.col_ptr + (valid ? j + 1 : bk.s1));
     double A = 0.0, w = 0.0;
     int kd = 0;
     if (valid) {  // independent of the gather: issue early
@@ -466,12 +390,11 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
     }
     const int span_beg = __shfl_sync(kFull, beg, 0);
     const int span_end = __shfl_sync(kFull, end, 31);
-    const int nspan_beg = has_next ? __shfl_sync(kFull, nbeg, 0) : -1;
-    const int nspan_end = has_next ? __shfl_sync(kFull, nend, 31) : -1;
-    const double sum = warp_segments_sum_chain(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
-                                               pol_first, buf, nspan_beg, nspan_end);
-    // keep the kind test (and the wait for the kind / weight loads) after
-    // the gather loop (see the tile body history in DESIGN.md)
+    const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
+                                         pol_first);
+    // keep the kind test (and with it the wait for the kind / weight loads)
+    // after the gather loop: the compiler otherwise hoists it and the warp
+    // stalls on those loads before issuing any gather
     asm volatile("" : "+r"(kd), "+d"(w) : : "memory");
     if (valid) {
       const int tau = end - beg;
@@ -485,8 +408,6 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
       p_tda2 += static_cast<double>(tau) * dA * dA;
       if (trace_it) p_obj += (kd == NUMPMP_KIND_LOG) ? w * log(x) : w * x;
     }
-    beg = nbeg;
-    end = nend;
   }
 }
 
