@@ -531,22 +531,42 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
 
 // The last CTA of a fused link pass: fixed-order sums of the stream-pass
 // and link-pass partials, then finalize_iteration.
+// One warp's fixed-order sum of part[i * stride + comp], i < count: lane l
+// adds i = l, l + 32, ... (4 loads in flight), then a butterfly.  The same
+// order on every call and every rank.
+__device__ __forceinline__ double warp_sum_array(const double* part, int count, int stride, int comp,
+                                                 int lane) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int i = lane;
+  for (; i + 96 < count; i += 128) {
+    s0 += __ldcg(part + (long long)i * stride + comp);
+    s1 += __ldcg(part + (long long)(i + 32) * stride + comp);
+    s2 += __ldcg(part + (long long)(i + 64) * stride + comp);
+    s3 += __ldcg(part + (long long)(i + 96) * stride + comp);
+  }
+  for (; i < count; i += 32) s0 += __ldcg(part + (long long)i * stride + comp);
+  return warp_sum((s0 + s1) + (s2 + s3));
+}
+
+// The last CTA of an iteration's link side: the six residual / objective
+// sums, one warp each, in parallel; then finalize_iteration.
 __device__ __forceinline__ void last_block_finalize(const IterArgs& a, double rho, int nparts,
                                                     bool scalars_in_lbuf) {
-  double tda2, obj;
-  if (scalars_in_lbuf) {
-    tda2 = __ldcg(a.Lbuf + a.m);
-    obj = __ldcg(a.Lbuf + a.m + 1);
-  } else {
-    tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
-    obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
-  }
-  const double r2 = block_sum_array(a.k2_part, nparts, 4, 0);
-  const double cross = block_sum_array(a.k2_part, nparts, 4, 1);
-  const double ddb2 = block_sum_array(a.k2_part, nparts, 4, 2);
-  const double dzs2 = block_sum_array(a.k2_part, nparts, 4, 3);
+  static_assert(kWarps >= 6, "one warp per sum");
+  __shared__ double sums[6];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int n1 = a.grid1 * a.nblocks;
+  double v = 0.0;
+  if (wib == 0)
+    v = scalars_in_lbuf ? __ldcg(a.Lbuf + a.m) : warp_sum_array(a.k1_part, n1, 2, 0, lane);
+  else if (wib == 1)
+    v = scalars_in_lbuf ? __ldcg(a.Lbuf + a.m + 1) : warp_sum_array(a.k1_part, n1, 2, 1, lane);
+  else if (wib < 6)
+    v = warp_sum_array(a.k2_part, nparts, 4, wib - 2, lane);
+  if (wib < 6 && lane == 0) sums[wib] = v;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    finalize_iteration(a, rho, tda2, obj, r2, cross, ddb2, dzs2);
+    finalize_iteration(a, rho, sums[0], sums[1], sums[2], sums[3], sums[4], sums[5]);
     a.ctrl->ticket = 0;
     __threadfence();
   }
