@@ -426,33 +426,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
 }
 
 // --------------------------------------------------------------- K2: links
-// Per-link epilogue: slack projection (solver.hpp:368-376), link average
-// (110-126), z update split into B / zs / Q (388-399), price (401-405).
-__device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, double L, int d,
-                                              double rho, double (&part)[4], uint64_t pol,
-                                              uint64_t pol_last, double* Bn_out = nullptr,
-                                              double* prn_out = nullptr) {
+struct LinkIn {  // one link's epilogue inputs
+  double c, pr, B, zs, Q;
+};
+__device__ __forceinline__ LinkIn load_link(const IterArgs& a, long long r, uint64_t pol) {
+  LinkIn in;
+  in.c = __ldg(a.cap + r);
+  in.pr = ld_stream_f64(a.pr_in + r, pol);
+  in.B = ld_stream_f64(a.B_in + r, pol);
+  in.zs = ld_stream_f64(a.zs_in + r, pol);
+  in.Q = ld_stream_f64(a.Q_in + r, pol);
+  return in;
+}
+__device__ __forceinline__ double link_update(const IterArgs& a, long long r, double L, int d,
+                                             const LinkIn& in, double rho, double (&part)[4],
+                                             uint64_t pol_last, double* Bn_out = nullptr,
+                                             double* prn_out = nullptr) {
   const double alpha = a.alpha;
-  const double c = __ldg(a.cap + r);
-  const double pr = ld_stream_f64(a.pr_in + r, pol);
-  const double B = ld_stream_f64(a.B_in + r, pol);
-  const double zs = ld_stream_f64(a.zs_in + r, pol);
-  const double Q = ld_stream_f64(a.Q_in + r, pol);
-  const double u = pr / rho;
-  const double ps = dmax_ref(zs - u, -c);
+  const double u = in.pr / rho;
+  const double ps = dmax_ref(in.zs - u, -in.c);
   const double cnt = static_cast<double>(d + 1);
   const double pbar = (L + ps) / cnt;
   part[0] += cnt * pbar * pbar;
-  const double Bn = alpha * pbar + (1.0 - alpha) * B;
-  const double dB = Bn - B;
-  const double zsn = alpha * (ps - pbar) + (1.0 - alpha) * zs;
-  const double dzs = zsn - zs;
-  const double Qn = alpha * L + (1.0 - alpha) * Q;
-  const double dQ = Qn - Q;
+  const double Bn = alpha * pbar + (1.0 - alpha) * in.B;
+  const double dB = Bn - in.B;
+  const double zsn = alpha * (ps - pbar) + (1.0 - alpha) * in.zs;
+  const double dzs = zsn - in.zs;
+  const double Qn = alpha * L + (1.0 - alpha) * in.Q;
+  const double dQ = Qn - in.Q;
   part[1] += dB * dQ;
   part[2] += static_cast<double>(d) * dB * dB;
   part[3] += dzs * dzs;
-  const double prn = pr + rho * (alpha * pbar);
+  const double prn = in.pr + rho * (alpha * pbar);
   a.B_out[r] = Bn;
   a.zs_out[r] = zsn;
   a.Q_out[r] = Qn;
@@ -469,6 +474,14 @@ __device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, 
     st_hint_f64(a.v_alt[1] + r, Bn + prn / (rho / a.gamma), pol_last);
   }
   return vn;
+}
+// Per-link epilogue: slack projection (solver.hpp:368-376), link average
+// (110-126), z update split into B / zs / Q (388-399), price (401-405).
+__device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, double L, int d,
+                                              double rho, double (&part)[4], uint64_t pol,
+                                              uint64_t pol_last, double* Bn_out = nullptr,
+                                              double* prn_out = nullptr) {
+  return link_update(a, r, L, d, load_link(a, r, pol), rho, part, pol_last, Bn_out, prn_out);
 }
 
 // Finalize one iteration on the device: r, s, then the exact control order
@@ -725,9 +738,25 @@ __global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
   const uint64_t pol_last = policy_evict_last();
   double part[4] = {0.0, 0.0, 0.0, 0.0};
   const double* L = (kSrc == 0) ? a.Lbuf : a.Lacc;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.m;
-       r += (long long)gridDim.x * blockDim.x)
-    link_epilogue(a, r, __ldcg(L + r), __ldg(a.deg + r), rho, part, pol_first, pol_last);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.m; r += 2 * stride) {
+    // two links' loads in flight per thread (same link order as one at a time)
+    const long long r1 = r + stride;
+    const bool has1 = r1 < a.m;
+    const LinkIn in0 = load_link(a, r, pol_first);
+    const double L0 = __ldcg(L + r);
+    const int d0 = __ldg(a.deg + r);
+    LinkIn in1{};
+    double L1 = 0.0;
+    int d1 = 0;
+    if (has1) {
+      in1 = load_link(a, r1, pol_first);
+      L1 = __ldcg(L + r1);
+      d1 = __ldg(a.deg + r1);
+    }
+    link_update(a, r, L0, d0, in0, rho, part, pol_last);
+    if (has1) link_update(a, r1, L1, d1, in1, rho, part, pol_last);
+  }
   block_sum_store<4>(part, a.k2_part + 4 * blockIdx.x);
   __threadfence();
   if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket, 1u) == gridDim.x - 1);
