@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "numpmp/common.hpp"
+#include "numpmp/gen.hpp"
 #include "numpmp/model.hpp"
 #include "numpmp/prox.hpp"
 #include "numpmp/solver.hpp"
@@ -128,6 +129,51 @@ class PmpSolver {
   Solution solve(const WarmStart& warm) {
     set_warm(warm);
     return run();
+  }
+
+  // warm.hpp:25-57 warm_start_after_degrade, computed on the device for this
+  // solver's (degraded) problem; `before` is the problem `prior` solved.
+  // The warm state is applied: solve_prepared() continues from it.  Returns
+  // the recipe's WarmStart (bit-identical to the reference function).
+  WarmStart warm_start_after_degrade(const Problem& before, const Solution& prior) {
+    if (before.m != prob_.m || before.n != prob_.n)
+      throw std::invalid_argument("degrade warm start: problems differ in structure");
+    WarmStart w;
+    w.x0.resize(static_cast<std::size_t>(prob_.n));
+    w.price.resize(static_cast<std::size_t>(prob_.m));
+    throw_on_error(numpmp_gpu_warm_after_degrade(h_, before.capacities.data(), prior.x.data(),
+                                                 prior.lambda_raw.data(), prior.rho_final,
+                                                 w.x0.data(), w.price.data(), &w.rho),
+                   h_);
+    return w;
+  }
+
+  // warm.hpp:62-94 warm_start_after_prune on the device (this solver holds
+  // the pruned problem); the PruneMap projection is a host gather.
+  WarmStart warm_start_after_prune(const PruneMap& map, const Solution& prior) {
+    const std::vector<double> x0 = map.project_streams(prior.x);
+    const std::vector<double> price = map.project_links(prior.lambda_raw);
+    if (std::int64_t(x0.size()) != prob_.n || std::int64_t(price.size()) != prob_.m)
+      throw std::invalid_argument("prune warm start: map does not fit problem");
+    WarmStart w;
+    w.x0.resize(x0.size());
+    w.price.resize(price.size());
+    throw_on_error(numpmp_gpu_warm_after_prune(h_, x0.data(), price.data(), prior.rho_final,
+                                               w.x0.data(), w.price.data(), &w.rho),
+                   h_);
+    return w;
+  }
+
+  // run() from the state the last warm-start recipe applied.
+  Solution solve_prepared() { return run(); }
+
+  // transit.hpp:290-302 path_prices on the device (route order).
+  std::vector<double> path_prices(const std::vector<double>& lambda) {
+    if (std::int64_t(lambda.size()) != prob_.m)
+      throw std::invalid_argument("path_prices: lambda length mismatch");
+    std::vector<double> pi(static_cast<std::size_t>(prob_.n));
+    throw_on_error(numpmp_gpu_path_prices(h_, lambda.data(), pi.data()), h_);
+    return pi;
   }
 
   const SolverState& final_state() {

@@ -151,6 +151,39 @@ int main() {
                   max_rel(b.x, a.x));
     check(a.iterations == b.iterations && max_rel(b.x, a.x) <= 1e-6 && 2 * b.iterations <= cold.iterations,
           buf);
+    // the same recipe on the device: bit-identical WarmStart, same re-solve
+    WarmStart wd = dev.warm_start_after_degrade(base, sol0);
+    Solution c = dev.solve_prepared();
+    std::snprintf(buf, sizeof buf, "device degrade recipe: x0/price/rho bit-identical %d, iterations %lld",
+                  int(wd.x0 == w.x0 && wd.price == w.price && wd.rho == w.rho), (long long)c.iterations);
+    check(wd.x0 == w.x0 && wd.price == w.price && wd.rho == w.rho && c.iterations == a.iterations, buf);
+  }
+  {  // warm.hpp:62-94 after link failures, host recipe vs device recipe
+    GenSpec spec;
+    spec.m = 300;
+    spec.n = 900;
+    spec.avg_links_per_stream = 4.0;
+    spec.kind = GenKind::Mixed;
+    spec.seed = 31;
+    Problem base = gen_uncongested(spec);
+    SolverConfig cfg;
+    cfg.eps_abs = 1e-5;
+    gpu::PmpSolver s0(base, cfg);
+    Solution sol0 = s0.solve();
+    auto [pruned, map] = fail_and_prune(base, 0.2, 6);
+    WarmStart w = warm_start_after_prune(pruned, map, sol0);
+    gpu::PmpSolver dev(pruned, cfg);
+    WarmStart wd = dev.warm_start_after_prune(map, sol0);
+    Solution c = dev.solve_prepared();
+    PmpSolver cpu(pruned, cfg);
+    Solution a = cpu.solve(w);
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "device prune recipe: bit-identical %d, iterations cpu %lld gpu %lld, x rel %.2e",
+                  int(wd.x0 == w.x0 && wd.price == w.price && wd.rho == w.rho), (long long)a.iterations,
+                  (long long)c.iterations, max_rel(c.x, a.x));
+    check(wd.x0 == w.x0 && wd.price == w.price && wd.rho == w.rho && a.iterations == c.iterations &&
+              max_rel(c.x, a.x) <= 1e-6,
+          buf);
   }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
