@@ -111,6 +111,8 @@ class ShardedPmpSolver:
             self.local, self.stream_begin = local_shard(problem, rank, world)
             return
         if exchange == "p2p":
+            if ipc_allgather is None:
+                raise ValueError('exchange="p2p" needs ipc_allgather (see the class docstring)')
             h, self.local, self.stream_begin = p2p_create(problem, config, rank, world, device)
             self._h = h
             handles = ipc_allgather(p2p_export(h))
@@ -119,6 +121,10 @@ class ShardedPmpSolver:
                 if rc:
                     raise_for(rc, L.numpmp_gpu_last_error(h).decode())
             return
+        if exchange != "nccl":
+            raise ValueError(f"unknown exchange {exchange!r} (p2p | nccl)")
+        if nccl_id is None:
+            raise ValueError('exchange="nccl" needs the broadcast nccl_id')
         self.local, self.stream_begin = local_shard(problem, rank, world)
         h = C.c_void_p()
         view = self.local.view()
