@@ -25,15 +25,27 @@ __global__ void k_validate(const long long* __restrict__ off, const int* __restr
   for (long long j = tid; j < n; j += stride) {
     const long long b = off[j], e = off[j + 1];
     if (e <= b) ++c[1];
+    // range check + strictly-increasing check in one pass (generated and
+    // most real routes are sorted); only an unsorted route pays the
+    // quadratic duplicate search.  Counts are flags: any nonzero count sends
+    // the caller to the host validator for the exact message.
+    bool sorted = true;
+    int prev = -1;
     for (long long t = b; t < e; ++t) {
       const int l = links[t];
       if (l < 0 || l >= m) ++c[2];
-      for (long long u = b; u < t; ++u)
-        if (links[u] == l) {
-          ++c[3];
-          break;
-        }
+      if (l <= prev) sorted = false;
+      prev = l;
     }
+    if (!sorted)
+      for (long long t = b; t < e; ++t) {
+        const int l = links[t];
+        for (long long u = b; u < t; ++u)
+          if (links[u] == l) {
+            ++c[3];
+            break;
+          }
+      }
     const double wj = w[j];
     const int k = kind[j];
     if (!isfinite(wj) || (k == NUMPMP_KIND_LOG && !(wj > 0.0)) || (k != NUMPMP_KIND_LOG && wj < 0.0))

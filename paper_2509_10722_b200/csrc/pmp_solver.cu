@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -92,6 +93,33 @@ const NcclApi& nccl() {
   } while (0)
 
 thread_local std::string g_create_err;
+
+// Pinned host slots for the control-block reads (2 Ctrl per handle), from a
+// process-wide free list: cudaMallocHost / cudaFreeHost per handle cost
+// milliseconds and synchronize the device.
+struct PinnedCtrlPool {
+  std::mutex mu;
+  std::vector<void*> free_slots;
+  void* get(size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!free_slots.empty()) {
+      void* p = free_slots.back();
+      free_slots.pop_back();
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+  }
+  void put(void* p) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_slots.push_back(p);
+  }
+};
+PinnedCtrlPool& ctrl_pool() {
+  static PinnedCtrlPool* pool = new PinnedCtrlPool();  // never destroyed: slots outlive handles
+  return *pool;
+}
 
 // Device memory comes from the device's stream-ordered pool, which is told
 // to keep freed memory reserved: creating and destroying solver handles
@@ -740,7 +768,8 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   h->scratch_n = dalloc<double>(static_cast<size_t>(n), b, h->stream);
   h->scalars = dalloc<double>(2, b, h->stream);
   h->ctrl = dalloc<Ctrl>(1, b, h->stream);
-  CK(cudaMallocHost(&h->ctrl_host, 2 * sizeof(Ctrl)));
+  h->ctrl_host = static_cast<Ctrl*>(ctrl_pool().get(2 * sizeof(Ctrl)));
+  if (!h->ctrl_host) throw GpuError{NUMPMP_CUDA_ERROR, "pinned host allocation failed"};
   CK(cudaMemsetAsync(h->row_idx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
   CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
 
@@ -1711,6 +1740,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
                              h->v_alt[0], h->v_alt[1],
                              h->Lbuf,    h->Lacc,    h->k1_part,   h->k2_part,    h->scratch_m,
                              h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
+  pt.mark("destroy: sync + ipc");
   for (int i = 0; i < 2; ++i) {
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
     for (int set = 0; set < 2; ++set)
@@ -1723,6 +1753,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
       bufs.push_back(p);
   }
   for (auto& e : h->prof_ev) cudaEventDestroy(e);
+  pt.mark("destroy: graphs + events");
   for (ColBlock& cb : h->blocks)
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
                     static_cast<void*>(cb.uptr), static_cast<void*>(cb.vptr),
@@ -1735,7 +1766,8 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
       else
         cudaFree(p);
     }
-  if (h->ctrl_host) cudaFreeHost(h->ctrl_host);
+  pt.mark("destroy: frees queued");
+  if (h->ctrl_host) ctrl_pool().put(h->ctrl_host);
   if (h->comm) nccl().CommDestroy(h->comm);
   for (cudaEvent_t e : h->pipe_ev)
     if (e) cudaEventDestroy(e);
