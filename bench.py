@@ -340,7 +340,7 @@ def run_ours(args):
     iter_gbs = (k1b + k2b) / (iter_ms * 1e-3) / 1e9
     # DRAM traffic of the dominant kernel per iteration, from the committed
     # ncu --set full capture (profiles/traffic_r1.json; config C, one GPU)
-    traffic, xbar_pct = None, None
+    traffic, xbar_pct, iter_dram = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic_r1.json")) as f:
             tr = json.load(f)
@@ -348,6 +348,7 @@ def run_ours(args):
             key = "k_link_pass" if avg2 >= avg1 else "k_stream_pass"
             traffic = tr["per_iteration"][key]["dram_bytes"]
             xbar_pct = tr["per_iteration"][key].get("xbar_req_pct")
+            iter_dram = sum(v["dram_bytes"] for v in tr["per_iteration"].values())
     except Exception:
         traffic = None
     # The structural bound: one random 8-byte gather per nonzero and pass,
@@ -461,7 +462,10 @@ def run_ours(args):
                                           "l1_to_l2_request_pct_ncu": xbar_pct,
                                           "source": "scripts/gather_lanes_bench.cu (profiles/r1_gather_lanes.txt); "
                                                     "request utilisation: profiles/traffic_r1.json"}},
-            "iteration_roofline": {"alg_bytes": k1b + k2b, "ms": iter_ms, "achieved_gbs": iter_gbs,
+            "iteration_roofline": {"alg_bytes": k1b + k2b, "alg_bytes_per_nnz": (k1b + k2b) / max(lp.nnz, 1),
+                                   "dram_bytes_ncu": iter_dram,
+                                   "dram_bytes_per_nnz_ncu": (iter_dram / max(lp.nnz, 1)) if iter_dram else None,
+                                   "ms": iter_ms, "achieved_gbs": iter_gbs,
                                    "frac": iter_gbs / hbm, "stream_pass_ms": avg1, "link_pass_ms": avg2},
             "gpu_launches": timed_launches + args.steps,
             "kernel_split": "per-launch CUDA events from one extra untimed solve of the serial graph",
