@@ -44,6 +44,10 @@ CONFIGS = {
               desc="D: C with 50% of capacities x0.5 (degrade seed 99)"),
     "E": dict(transit=(100, 192, 5.0, 952, 9900, 9, 192, 50.0, 4), rho0=1000.0,
               desc="E: time-expanded transit, S=100 T=192 |E|=952, 9900 OD x 9 routes x 192 departures, seats 50"),
+    # SURVEY.md 8(d) optional paper-shape cross-check (1847 s on an A100, tolerance and
+    # iteration count unstated): more links than streams
+    "P": dict(m=10000000, n=5000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
+              desc="P: paper shape, 5M streams / 10M links, log, w=1"),
 }
 
 
