@@ -166,6 +166,12 @@ struct BlockArgs {
   long long nv, nu;
   int index;           // block number b
   int first;           // b == 0
+  // row mode (blocks whose longest row is short, e.g. more links than
+  // streams): one lane per row, 32 consecutive rows per warp, no segment
+  // metadata and no scan
+  int row_mode;
+  const int* row_ptr;  // m+1 (this block's CSR)
+  long long m;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -631,42 +637,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   const uint64_t pol_last = policy_evict_last();
   const double rho = (kPhase == LP_FUSED) ? a.ctrl->rho : 0.0;
   double part[4] = {0.0, 0.0, 0.0, 0.0};
-  const long long ustride = (long long)gridDim.x * kWarps;
-  long long u = (long long)blockIdx.x * kWarps + wib;
-  // this unit's segment range, loaded one unit ahead (the uptr -> vptr chain
-  // would otherwise put two dependent loads in front of every unit)
-  int v0 = 0, v1 = 0;
-  if (u < bk.nu) {
-    v0 = __ldg(bk.uptr + u);
-    v1 = __ldg(bk.uptr + u + 1);
-  }
-  for (; u < bk.nu; u += ustride) {
-    const int v = v0 + lane;
-    const bool valid = v < v1;
-    // independent loads, no select on a loaded value (it would hold the
-    // next load back until the first one returns)
-    const int vb = __ldg(bk.vptr + (valid ? v : v1));
-    const int ve = __ldg(bk.vptr + (valid ? v + 1 : v1));
-    int row = -1 - lane;
-    if (valid) row = __ldg(bk.vrow + v);
-    if (u + ustride < bk.nu) {
-      v0 = __ldg(bk.uptr + u + ustride);
-      v1 = __ldg(bk.uptr + u + ustride + 1);
-    }
-    const int span_beg = __shfl_sync(kFull, vb, 0);
-    const int span_end = __shfl_sync(kFull, ve, 31);
-    double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
-                                 GatherX{src}, pol_first);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
-      const double t = __shfl_up_sync(kFull, s, d);
-      const int tr = __shfl_up_sync(kFull, row, d);
-      if (lane >= d && tr == row) s += t;
-    }
-    const int next_row = __shfl_down_sync(kFull, row, 1);
-    if (!valid || (lane != 31 && next_row == row)) continue;  // not the row's tail
-    const long long r = row;
-    const double L = bk.first ? s : __ldcg(a.Lacc + r) + s;
+  // a row's action once its load (this block's part added) is known
+  auto row_done = [&](long long r, double L) {
     if (kPhase == LP_ACC) {
       __stcg(a.Lacc + r, L);
     } else if (kPhase == LP_ROWSUM) {
@@ -679,6 +651,61 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       dst[a.p2p.rank * a.p2p.mo + (r - q * a.p2p.mo)] = L;
     } else {
       link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
+    }
+  };
+  if (bk.row_mode) {
+    const long long ngroups = (bk.m + 31) / 32;
+    for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
+         g += (long long)gridDim.x * kWarps) {
+      const long long r = g * 32 + lane;
+      const bool valid = r < bk.m;
+      const int rb = __ldg(bk.row_ptr + (valid ? r : bk.m));
+      const int re = __ldg(bk.row_ptr + (valid ? r + 1 : bk.m));
+      double Lprev = 0.0;
+      if (!bk.first && valid) Lprev = __ldcg(a.Lacc + r);
+      const int span_beg = __shfl_sync(kFull, rb, 0);
+      const int span_end = __shfl_sync(kFull, re, 31);
+      const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
+                                         GatherX{src}, pol_first);
+      if (valid) row_done(r, bk.first ? s : Lprev + s);
+    }
+  } else {
+    const long long ustride = (long long)gridDim.x * kWarps;
+    long long u = (long long)blockIdx.x * kWarps + wib;
+    // this unit's segment range, loaded one unit ahead (the uptr -> vptr chain
+    // would otherwise put two dependent loads in front of every unit)
+    int v0 = 0, v1 = 0;
+    if (u < bk.nu) {
+      v0 = __ldg(bk.uptr + u);
+      v1 = __ldg(bk.uptr + u + 1);
+    }
+    for (; u < bk.nu; u += ustride) {
+      const int v = v0 + lane;
+      const bool valid = v < v1;
+      // independent loads, no select on a loaded value (it would hold the
+      // next load back until the first one returns)
+      const int vb = __ldg(bk.vptr + (valid ? v : v1));
+      const int ve = __ldg(bk.vptr + (valid ? v + 1 : v1));
+      int row = -1 - lane;
+      if (valid) row = __ldg(bk.vrow + v);
+      if (u + ustride < bk.nu) {
+        v0 = __ldg(bk.uptr + u + ustride);
+        v1 = __ldg(bk.uptr + u + ustride + 1);
+      }
+      const int span_beg = __shfl_sync(kFull, vb, 0);
+      const int span_end = __shfl_sync(kFull, ve, 31);
+      double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
+                                   GatherX{src}, pol_first);
+  #pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
+        const double t = __shfl_up_sync(kFull, s, d);
+        const int tr = __shfl_up_sync(kFull, row, d);
+        if (lane >= d && tr == row) s += t;
+      }
+      const int next_row = __shfl_down_sync(kFull, row, 1);
+      if (!valid || (lane != 31 && next_row == row)) continue;  // not the row's tail
+      const long long r = row;
+      row_done(r, bk.first ? s : __ldcg(a.Lacc + r) + s);
     }
   }
   if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;

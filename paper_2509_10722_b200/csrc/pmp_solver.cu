@@ -175,6 +175,7 @@ struct ColBlock {
   int* uptr = nullptr;        // nu+1: first segment of each warp unit
   int64_t nu = 0;
   int seg = 0;                // max entries per segment
+  int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
 };
 
 }  // namespace
@@ -380,6 +381,9 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.nu = cb.nu;
   k.index = b;
   k.first = b == 0;
+  k.row_mode = cb.row_mode;
+  k.row_ptr = cb.row_ptr;
+  k.m = h->m;
   return k;
 }
 
@@ -671,6 +675,11 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   CK(cudaStreamSynchronize(h->stream));
   cudaFreeAsync(dmax, h->stream);
   cb.seg = std::max(kSeg, (maxd + 31) / 32);
+  // Row mode when the longest row is short: a lane per row costs no
+  // segment metadata or scan (NUMPMP_ROW_MODE_MAX, default 16 entries).
+  int row_mode_max = 16;
+  if (const char* env = std::getenv("NUMPMP_ROW_MODE_MAX")) row_mode_max = std::atoi(env);
+  cb.row_mode = maxd <= row_mode_max ? 1 : 0;
   int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
   int* row_vstart = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
   CK(cudaMemsetAsync(nseg + m, 0, sizeof(int), h->stream));
@@ -845,7 +854,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
-    max_nu = std::max(max_nu, cb.nu);
+    max_nu = std::max(max_nu, cb.row_mode ? (m + 31) / 32 : cb.nu);
   }
   const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
   h->grid1 = static_cast<int>(std::max(

@@ -751,3 +751,21 @@ def test_skewed_and_ragged_shapes_match_oracle(shape, blocks, restatement, oracl
         ok, err = close(got, want)
         assert ok, err
     assert abs(sol.objective - ref.objective) <= RTOL * abs(ref.objective)
+
+
+@pytest.mark.parametrize("row_mode_max", ["0", "100000"])
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restatement, oracle_mod, monkeypatch):
+    # the link pass's two forms (lane per row / warp units of segments) on the
+    # same problem: every block forced into one of them
+    monkeypatch.setenv("NUMPMP_ROW_MODE_MAX", row_mode_max)
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", str(blocks))
+    p = _gen(3000, 2000, 6.0, 2, True, 19)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
