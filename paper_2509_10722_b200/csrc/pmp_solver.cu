@@ -676,8 +676,10 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   cudaFreeAsync(dmax, h->stream);
   cb.seg = std::max(kSeg, (maxd + 31) / 32);
   // Row mode when the longest row is short: a lane per row costs no
-  // segment metadata or scan (NUMPMP_ROW_MODE_MAX, default 16 entries).
-  int row_mode_max = 16;
+  // segment metadata or scan.  NUMPMP_ROW_MODE_MAX, default 64 entries
+  // (C: -1.8%, P: -8%; B with 100-entry rows stays in units,
+  // profiles/r1_row_mode_sweep.txt).
+  int row_mode_max = 64;
   if (const char* env = std::getenv("NUMPMP_ROW_MODE_MAX")) row_mode_max = std::atoi(env);
   cb.row_mode = maxd <= row_mode_max ? 1 : 0;
   int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
