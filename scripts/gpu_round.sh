@@ -15,7 +15,7 @@ for c in B E D; do
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -c 2000 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_stream_pass|k_link_pass|k_link_epilogue|k_refresh_v" -s 9 -c 9 -o gpurun_out/prof_c_$TAG -f python scripts/profile_run.py C 6 > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_stream_pass|k_link_pass|k_link_epilogue|k_refresh_v" -s 10 -c 9 -o gpurun_out/prof_c_$TAG -f python scripts/profile_run.py C 6 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -n 3 gpurun_out/pytest_gpu_$TAG.log; tail -n 2 gpurun_out/dropin_$TAG.log; tail -n 2 gpurun_out/ncu_launch_$TAG.log gpurun_out/ncu_full_$TAG.log
 for c in C B E D; do python -c "
 import json

@@ -21,10 +21,8 @@ def val(d, m):
     return float(d[ix[m]]) * scale.get(units[ix[m]], 1.0)
 
 
-# one iteration starts at the first stream pass (drop a leading epilogue of
-# the previous iteration if the capture window caught one)
-while data and "stream_pass" not in data[0][ix["Kernel Name"]]:
-    data = data[1:]
+# The capture window holds one iteration's worth of launches (NB stream
+# passes, NB link passes, one epilogue), possibly straddling two iterations.
 per = {}
 for d in data:
     name = d[ix["Kernel Name"]].split("(")[0].replace("void ", "").split("<")[0].replace("numpmp_dev::", "")
