@@ -170,6 +170,7 @@ struct BlockArgs {
   // streams): one lane per row, 32 consecutive rows per warp, no segment
   // metadata and no scan
   int row_mode;
+  int pair_tiles;      // k_stream_pass on 64-stream pair tiles (short routes)
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
 };
@@ -298,6 +299,60 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
   return acc;
 }
 
+// warp_segments_sum with two segments per lane ([b0, e0) and [b1, e1), b1 >= e0
+// across the warp): each batch issues kUnroll/2 gathers from each segment, so
+// a lane with two short routes keeps both in flight at once.  Each segment
+// is summed in index order.
+template <class G>
+__device__ __forceinline__ void warp_segments_sum2(const int* __restrict__ idx, int span_beg,
+                                                   int span_end, int b0, int e0, int b1, int e1,
+                                                   int* __restrict__ sidx, int lane, G g,
+                                                   uint64_t pol_stream, double& acc0, double& acc1) {
+  constexpr int NV = kStageInts / 128;
+  constexpr int H = kUnroll / 2;
+  acc0 = 0.0;
+  acc1 = 0.0;
+  int cb = span_beg & ~3;
+  int4 buf[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int gp = cb + 4 * (lane + 32 * i);
+    if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
+  }
+  while (cb < span_end) {
+    const int c1 = min(cb + kStageInts, span_end);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int o = 4 * (lane + 32 * i);
+      if (cb + o < c1) *reinterpret_cast<int4*>(sidx + o) = buf[i];
+    }
+    __syncwarp();
+    const int nb = cb + kStageInts;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int gp = nb + 4 * (lane + 32 * i);
+      if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
+    }
+    const int lo0 = max(b0, cb), hi0 = min(e0, c1);
+    const int lo1 = max(b1, cb), hi1 = min(e1, c1);
+    for (int k0 = lo0, k1 = lo1; k0 < hi0 || k1 < hi1; k0 += H, k1 += H) {
+      double va[H], vb[H];
+#pragma unroll
+      for (int u = 0; u < H; ++u) {
+        va[u] = (k0 + u < hi0) ? g(sidx[k0 + u - cb]) : 0.0;
+        vb[u] = (k1 + u < hi1) ? g(sidx[k1 + u - cb]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < H; ++u) {
+        if (k0 + u < hi0) acc0 += va[u];
+        if (k1 + u < hi1) acc1 += vb[u];
+      }
+    }
+    __syncwarp();
+    cb = nb;
+  }
+}
+
 // Fixed-order block reduction of NV partials; thread 0 writes out[0..NV).
 template <int NV>
 __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* out) {
@@ -417,6 +472,65 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
   }
 }
 
+// Pair tiles (short routes, e.g. the transit instance's ~3 links): a warp
+// takes 64 consecutive streams, lane l streams l and l + 32, both routes'
+// gathers in the same batches -- twice the work behind each tile's chain of
+// dependent loads (offsets, index staging, gathers).
+__device__ __forceinline__ void stream_update(const IterArgs& a, long long j, int beg, int end,
+                                              double A, double w, int kd, double sum, double rho,
+                                              bool trace_it, double& p_tda2, double& p_obj,
+                                              uint64_t pol_first, uint64_t pol_last) {
+  const int tau = end - beg;
+  const double zeta = static_cast<double>(tau) * A - sum;
+  const double x = (kd == NUMPMP_KIND_LOG) ? prox_log(zeta, w, rho, tau)
+                                           : prox_linear_nonneg(zeta, w, rho, tau);
+  const double An = a.alpha * x + (1.0 - a.alpha) * A;
+  const double dA = An - A;
+  st_hint_f64(a.x + j, x, pol_last);
+  st_hint_f64(a.A_out + j, An, pol_first);
+  p_tda2 += static_cast<double>(tau) * dA * dA;
+  if (trace_it) p_obj += (kd == NUMPMP_KIND_LOG) ? w * log(x) : w * x;
+}
+
+template <class G>
+__device__ __forceinline__ void stream_pass_pairs(const IterArgs& a, const BlockArgs& bk, G g,
+                                                  double rho, bool trace_it, int* sidx,
+                                                  double& p_tda2, double& p_obj) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last();
+  const long long npairs = (bk.s1 - bk.s0 + 63) / 64;
+  for (long long pt = (long long)blockIdx.x * kWarps + wib; pt < npairs;
+       pt += (long long)gridDim.x * kWarps) {
+    const long long j0 = bk.s0 + pt * 64 + lane, j1 = j0 + 32;
+    const bool v0 = j0 < bk.s1, v1 = j1 < bk.s1;
+    const int beg0 = __ldg(a.col_ptr + (v0 ? j0 : bk.s1));
+    const int end0 = __ldg(a.col_ptr + (v0 ? j0 + 1 : bk.s1));
+    const int beg1 = __ldg(a.col_ptr + (v1 ? j1 : bk.s1));
+    const int end1 = __ldg(a.col_ptr + (v1 ? j1 + 1 : bk.s1));
+    double A0 = 0.0, w0 = 0.0, A1 = 0.0, w1 = 0.0;
+    int kd0 = 0, kd1 = 0;
+    if (v0) {
+      A0 = ld_stream_f64(a.A_in + j0, pol_first);
+      w0 = __ldg(a.w + j0);
+      kd0 = __ldg(a.kind + j0);
+    }
+    if (v1) {
+      A1 = ld_stream_f64(a.A_in + j1, pol_first);
+      w1 = __ldg(a.w + j1);
+      kd1 = __ldg(a.kind + j1);
+    }
+    const int span_beg = __shfl_sync(kFull, beg0, 0);
+    const int span_end = max(__shfl_sync(kFull, end0, 31), __shfl_sync(kFull, end1, 31));
+    double s0, s1;
+    warp_segments_sum2(a.row_idx, span_beg, span_end, beg0, end0, beg1, end1, sidx, lane, g,
+                       pol_first, s0, s1);
+    asm volatile("" : "+r"(kd0), "+d"(w0), "+r"(kd1), "+d"(w1) : : "memory");
+    if (v0) stream_update(a, j0, beg0, end0, A0, w0, kd0, s0, rho, trace_it, p_tda2, p_obj, pol_first, pol_last);
+    if (v1) stream_update(a, j1, beg1, end1, A1, w1, kd1, s1, rho, trace_it, p_tda2, p_obj, pol_first, pol_last);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
   __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
@@ -427,7 +541,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   int* sb = sidx[threadIdx.x >> 5];
   const int sel = a.ctrl->v_sel;
   const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
+  if (bk.pair_tiles)
+    stream_pass_pairs(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
+  else
+    stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 

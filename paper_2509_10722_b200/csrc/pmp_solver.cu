@@ -176,6 +176,7 @@ struct ColBlock {
   int64_t nu = 0;
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
+  int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
 };
 
 }  // namespace
@@ -382,6 +383,7 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.index = b;
   k.first = b == 0;
   k.row_mode = cb.row_mode;
+  k.pair_tiles = cb.pair_tiles;
   k.row_ptr = cb.row_ptr;
   k.m = h->m;
   return k;
@@ -838,6 +840,11 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     cb.col_idx = dalloc<int>(static_cast<size_t>(cb.nnz) + kIdxPad, b, h->stream);
     h->blocks.push_back(cb);
     build_csr(h, cb.s0, cb.s1, cb.row_ptr, cb.col_idx, nullptr);
+    // pair tiles for short routes: mean route length <= NUMPMP_PAIR_TILE_TAU (default 6)
+    double pair_tau = 6.0;
+    if (const char* env = std::getenv("NUMPMP_PAIR_TILE_TAU")) pair_tau = std::atof(env);
+    h->blocks.back().pair_tiles =
+        (cb.s1 > cb.s0 && static_cast<double>(cb.nnz) <= pair_tau * static_cast<double>(cb.s1 - cb.s0)) ? 1 : 0;
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
     CK(cudaGetLastError());
     segment_block(h, h->blocks.back());

@@ -769,3 +769,20 @@ def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restate
     for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
         ok, err = close(got, want)
         assert ok, err
+
+
+@pytest.mark.parametrize("pair_tau", ["0", "100"])
+def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, restatement, oracle_mod, monkeypatch):
+    # the stream pass on 32-stream tiles and on 64-stream pair tiles (two
+    # routes per lane), forced; transit-like short routes and a ragged tail
+    monkeypatch.setenv("NUMPMP_PAIR_TILE_TAU", pair_tau)
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", "2")
+    p, _ = pmp.gen_transit(pmp.TransitSpec(12, 24, 5.0, 40, 30, 3, 6, 50.0, 2))
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=10.0)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw)]:
+        ok, err = close(got, want)
+        assert ok, err
