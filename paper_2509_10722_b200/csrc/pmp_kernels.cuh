@@ -531,6 +531,9 @@ __device__ __forceinline__ void stream_pass_pairs(const IterArgs& a, const Block
   }
 }
 
+// kPairs: pair tiles (short routes) -- a separate instantiation, so the tile
+// form keeps its own register allocation.
+template <bool kPairs>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
   __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
@@ -541,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   int* sb = sidx[threadIdx.x >> 5];
   const int sel = a.ctrl->v_sel;
   const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  if (bk.pair_tiles)
+  if (kPairs)
     stream_pass_pairs(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   else
     stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);

@@ -429,7 +429,10 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    k_stream_pass<<<h->grid1, kThreads, 0, s1>>>(a, bk);
+    if (bk.pair_tiles)
+      k_stream_pass<true><<<h->grid1, kThreads, 0, s1>>>(a, bk);
+    else
+      k_stream_pass<false><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     mark(1);
     if (pipelined) {
       CK(cudaEventRecord(ev_k1[b], h->stream2));
@@ -856,7 +859,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<false>, kThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
   int occ3 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
