@@ -433,30 +433,15 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
   const long long ntiles = (bk.s1 - bk.s0 + 31) / 32;
-  const long long tstride = (long long)gridDim.x * kWarps;
   const double alpha = a.alpha;
-  // a tile's offsets are loaded one tile ahead (two registers): the gathers
-  // of a tile cannot start before its span is known
-  long long tile = (long long)blockIdx.x * kWarps + wib;
-  int nbeg = 0, nend = 0;
-  if (tile < ntiles) {
+  for (long long tile = (long long)blockIdx.x * kWarps + wib; tile < ntiles;
+       tile += (long long)gridDim.x * kWarps) {
     const long long j = bk.s0 + tile * 32 + lane;
     const bool valid = j < bk.s1;
     // two independent offset loads (no select on a loaded value, so the
     // second load is not held back by the first)
-    nbeg = __ldg(a.col_ptr + (valid ? j : bk.s1));
-    nend = __ldg(a.col_ptr + (valid ? j + 1 : bk.s1));
-  }
-  for (; tile < ntiles; tile += tstride) {
-    const long long j = bk.s0 + tile * 32 + lane;
-    const bool valid = j < bk.s1;
-    const int beg = nbeg, end = nend;
-    if (tile + tstride < ntiles) {
-      const long long jn = j + 32 * tstride;
-      const bool vn = jn < bk.s1;
-      nbeg = __ldg(a.col_ptr + (vn ? jn : bk.s1));
-      nend = __ldg(a.col_ptr + (vn ? jn + 1 : bk.s1));
-    }
+    const int beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
+    const int end = __ldg(a.col_ptr + (valid ? j + 1 : bk.s1));
     double A = 0.0, w = 0.0;
     int kd = 0;
     if (valid) {  // independent of the gather: issue early
