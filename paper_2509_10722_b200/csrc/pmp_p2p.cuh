@@ -91,16 +91,13 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
   const double* slots = ld_ptr(p.slots_peer + p.rank);
   // rho-update iteration: v for both candidate rhos too (finalize picks one)
   const bool cand = a.mode == MODE_RUN && (a.ctrl->run_k + 1) % a.rho_interval == 0;
-  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1;
-       l += (long long)gridDim.x * blockDim.x) {
-    double L = 0.0;
-    for (int q = 0; q < p.world; ++q) L += __ldcg(slots + q * p.mo + (l - p.l0));
+  auto finish = [&](long long l, double L, int d, const LinkIn& in) {
     double Bn, prn;
-    const double v = link_epilogue(a, l, L, __ldg(a.deg + l), rho, part, pol_first, pol_last, &Bn, &prn);
+    const double v = link_update(a, l, L, d, in, rho, part, pol_last, &Bn, &prn);
     const double vu = cand ? Bn + prn / (rho * a.gamma) : 0.0;
     const double vd = cand ? Bn + prn / (rho / a.gamma) : 0.0;
     for (int q = 0; q < p.world; ++q) {
-      if (q == p.rank) continue;  // local copies written by link_epilogue
+      if (q == p.rank) continue;  // local copies written by link_update
       double* vq = ld_ptr(p.v_peer + q);
       vq[l] = v;
       if (cand) {
@@ -108,6 +105,27 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
         vq[2 * a.m + l] = vd;
       }
     }
+  };
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long l = p.l0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; l < p.l1; l += 2 * stride) {
+    // two links' loads in flight per thread (same link order as one at a time)
+    const long long l1 = l + stride;
+    const bool has1 = l1 < p.l1;
+    const LinkIn in0 = load_link(a, l, pol_first);
+    const int d0 = __ldg(a.deg + l);
+    LinkIn in1{};
+    int d1 = 0;
+    if (has1) {
+      in1 = load_link(a, l1, pol_first);
+      d1 = __ldg(a.deg + l1);
+    }
+    double L0 = 0.0, L1 = 0.0;  // the ranks' partial loads, rank order
+    for (int q = 0; q < p.world; ++q) {
+      L0 += __ldcg(slots + q * p.mo + (l - p.l0));
+      if (has1) L1 += __ldcg(slots + q * p.mo + (l1 - p.l0));
+    }
+    finish(l, L0, d0, in0);
+    if (has1) finish(l1, L1, d1, in1);
   }
   block_sum_store<4>(part, p.ep_part + 4 * blockIdx.x);
   __threadfence_system();
