@@ -687,6 +687,18 @@ __device__ __forceinline__ double warp_sum_array(const double* part, int count, 
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
+// Components 0..ncomp-1 (ncomp <= kWarps) of a strided partial array, one
+// warp each in parallel, fixed order; every thread gets res[0..ncomp).
+__device__ __forceinline__ void multi_sum(const double* part, int count, int stride, int ncomp,
+                                          double* res /* shared, >= ncomp */) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (wib < ncomp) {
+    const double v = warp_sum_array(part, count, stride, wib, lane);
+    if (lane == 0) res[wib] = v;
+  }
+  __syncthreads();
+}
+
 // The last CTA of an iteration's link side: the six residual / objective
 // sums, one warp each, in parallel; then finalize_iteration.
 __device__ __forceinline__ void last_block_finalize(const IterArgs& a, double rho, int nparts,
@@ -836,11 +848,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
     __syncthreads();
     if (!s_last) return;
     __threadfence_system();
-    const double tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
-    const double obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
+    __shared__ double k1s[2];
+    multi_sum(a.k1_part, a.grid1 * a.nblocks, 2, 2, k1s);
     if (threadIdx.x == 0) {
-      a.p2p.k1_scalars[0] = tda2;
-      a.p2p.k1_scalars[1] = obj;
+      a.p2p.k1_scalars[0] = k1s[0];
+      a.p2p.k1_scalars[1] = k1s[1];
       a.ctrl->ticket2 = 0;
       __threadfence_system();
       for (int q = 0; q < a.p2p.world; ++q) signal_sys(a.p2p.flags_peer[q] + 0);  // "loads stored"
@@ -854,11 +866,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const double tda2 = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 0);
-    const double obj = block_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, 1);
+    __shared__ double k1s[2];
+    multi_sum(a.k1_part, a.grid1 * a.nblocks, 2, 2, k1s);
     if (threadIdx.x == 0) {
-      a.Lbuf[a.m] = tda2;
-      a.Lbuf[a.m + 1] = obj;
+      a.Lbuf[a.m] = k1s[0];
+      a.Lbuf[a.m + 1] = k1s[1];
       a.ctrl->ticket2 = 0;
     }
     return;

@@ -134,12 +134,10 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const double r2 = block_sum_array(p.ep_part, gridDim.x, 4, 0);
-  const double cross = block_sum_array(p.ep_part, gridDim.x, 4, 1);
-  const double ddb2 = block_sum_array(p.ep_part, gridDim.x, 4, 2);
-  const double dzs2 = block_sum_array(p.ep_part, gridDim.x, 4, 3);
+  __shared__ double eps[4];
+  multi_sum(p.ep_part, gridDim.x, 4, 4, eps);
   if (threadIdx.x == 0) {
-    const double row[6] = {__ldcg(p.k1_scalars), __ldcg(p.k1_scalars + 1), r2, cross, ddb2, dzs2};
+    const double row[6] = {__ldcg(p.k1_scalars), __ldcg(p.k1_scalars + 1), eps[0], eps[1], eps[2], eps[3]};
     for (int q = 0; q < p.world; ++q) {
       double* xs = ld_ptr(p.xs_peer + q) + 8 * p.rank;
       for (int i = 0; i < 6; ++i) xs[i] = row[i];
