@@ -842,9 +842,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   }
   if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;
   if (kPhase == LP_P2P) {
-    __threadfence_system();  // this thread's peer stores, before the ticket
+    // The CTA's peer stores, then one system-scope fence before the ticket
+    // (the grid.sync pattern: bar.sync orders the CTA's writes before thread
+    // 0's cumulative fence).
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket2, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      s_last = (atomicAdd(&a.ctrl->ticket2, 1u) == gridDim.x - 1);
+    }
     __syncthreads();
     if (!s_last) return;
     __threadfence_system();

@@ -127,10 +127,11 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
     finish(l, L0, d0, in0);
     if (has1) finish(l1, L1, d1, in1);
   }
-  block_sum_store<4>(part, p.ep_part + 4 * blockIdx.x);
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&a.ctrl->ticket3, 1u) == gridDim.x - 1);
+  block_sum_store<4>(part, p.ep_part + 4 * blockIdx.x);  // ends with bar.sync
+  if (threadIdx.x == 0) {  // one cumulative system-scope fence per CTA (grid.sync pattern)
+    __threadfence_system();
+    s_last = (atomicAdd(&a.ctrl->ticket3, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
