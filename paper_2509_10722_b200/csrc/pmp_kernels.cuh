@@ -170,7 +170,7 @@ struct BlockArgs {
   // streams): one lane per row, 32 consecutive rows per warp, no segment
   // metadata and no scan
   int row_mode;
-  int pair_tiles;      // k_stream_pass on 64-stream pair tiles (short routes)
+  int pair_tiles;      // k_stream_pass streams per lane (1 = tiles; 2 / 4 for short routes)
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
 };
@@ -299,19 +299,19 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
   return acc;
 }
 
-// warp_segments_sum with two segments per lane ([b0, e0) and [b1, e1), b1 >= e0
-// across the warp): each batch issues kUnroll/2 gathers from each segment, so
-// a lane with two short routes keeps both in flight at once.  Each segment
-// is summed in index order.
-template <class G>
-__device__ __forceinline__ void warp_segments_sum2(const int* __restrict__ idx, int span_beg,
-                                                   int span_end, int b0, int e0, int b1, int e1,
-                                                   int* __restrict__ sidx, int lane, G g,
-                                                   uint64_t pol_stream, double& acc0, double& acc1) {
+// warp_segments_sum with Q segments per lane ([b[q], e[q]), lane-ordered
+// within each q, segment q+1 after segment q across the warp): each batch
+// issues kUnroll/Q gathers from every segment, so a lane with Q short routes
+// keeps all of them in flight at once.  Each segment is summed in index order.
+template <int Q, class G>
+__device__ __forceinline__ void warp_segments_sum_q(const int* __restrict__ idx, int span_beg,
+                                                    int span_end, const int (&b)[Q], const int (&e)[Q],
+                                                    int* __restrict__ sidx, int lane, G g,
+                                                    uint64_t pol_stream, double (&acc)[Q]) {
   constexpr int NV = kStageInts / 128;
-  constexpr int H = kUnroll / 2;
-  acc0 = 0.0;
-  acc1 = 0.0;
+  constexpr int H = kUnroll / Q;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
   int cb = span_beg & ~3;
   int4 buf[NV];
 #pragma unroll
@@ -333,19 +333,28 @@ __device__ __forceinline__ void warp_segments_sum2(const int* __restrict__ idx, 
       const int gp = nb + 4 * (lane + 32 * i);
       if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
     }
-    const int lo0 = max(b0, cb), hi0 = min(e0, c1);
-    const int lo1 = max(b1, cb), hi1 = min(e1, c1);
-    for (int k0 = lo0, k1 = lo1; k0 < hi0 || k1 < hi1; k0 += H, k1 += H) {
-      double va[H], vb[H];
+    int k[Q], hi[Q];
+    bool more = false;
 #pragma unroll
-      for (int u = 0; u < H; ++u) {
-        va[u] = (k0 + u < hi0) ? g(sidx[k0 + u - cb]) : 0.0;
-        vb[u] = (k1 + u < hi1) ? g(sidx[k1 + u - cb]) : 0.0;
-      }
+    for (int q = 0; q < Q; ++q) {
+      k[q] = max(b[q], cb);
+      hi[q] = min(e[q], c1);
+      more = more || k[q] < hi[q];
+    }
+    while (more) {
+      double vv[Q][H];
 #pragma unroll
-      for (int u = 0; u < H; ++u) {
-        if (k0 + u < hi0) acc0 += va[u];
-        if (k1 + u < hi1) acc1 += vb[u];
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int u = 0; u < H; ++u) vv[q][u] = (k[q] + u < hi[q]) ? g(sidx[k[q] + u - cb]) : 0.0;
+      more = false;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+#pragma unroll
+        for (int u = 0; u < H; ++u)
+          if (k[q] + u < hi[q]) acc[q] += vv[q][u];
+        k[q] += H;
+        more = more || k[q] < hi[q];
       }
     }
     __syncwarp();
@@ -472,10 +481,10 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
   }
 }
 
-// Pair tiles (short routes, e.g. the transit instance's ~3 links): a warp
-// takes 64 consecutive streams, lane l streams l and l + 32, both routes'
-// gathers in the same batches -- twice the work behind each tile's chain of
-// dependent loads (offsets, index staging, gathers).
+// Multi-route tiles (short routes, e.g. the transit instance's ~3 links): a
+// warp takes 32*Q consecutive streams, lane l streams l, l + 32, ..., all Q
+// routes' gathers in the same batches -- Q times the work behind each tile's
+// chain of dependent loads (offsets, index staging, gathers).
 __device__ __forceinline__ void stream_update(const IterArgs& a, long long j, int beg, int end,
                                               double A, double w, int kd, double sum, double rho,
                                               bool trace_it, double& p_tda2, double& p_obj,
@@ -492,48 +501,53 @@ __device__ __forceinline__ void stream_update(const IterArgs& a, long long j, in
   if (trace_it) p_obj += (kd == NUMPMP_KIND_LOG) ? w * log(x) : w * x;
 }
 
-template <class G>
-__device__ __forceinline__ void stream_pass_pairs(const IterArgs& a, const BlockArgs& bk, G g,
+template <int Q, class G>
+__device__ __forceinline__ void stream_pass_multi(const IterArgs& a, const BlockArgs& bk, G g,
                                                   double rho, bool trace_it, int* sidx,
                                                   double& p_tda2, double& p_obj) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
-  const long long npairs = (bk.s1 - bk.s0 + 63) / 64;
-  for (long long pt = (long long)blockIdx.x * kWarps + wib; pt < npairs;
+  const long long ngroups = (bk.s1 - bk.s0 + 32 * Q - 1) / (32 * Q);
+  for (long long pt = (long long)blockIdx.x * kWarps + wib; pt < ngroups;
        pt += (long long)gridDim.x * kWarps) {
-    const long long j0 = bk.s0 + pt * 64 + lane, j1 = j0 + 32;
-    const bool v0 = j0 < bk.s1, v1 = j1 < bk.s1;
-    const int beg0 = __ldg(a.col_ptr + (v0 ? j0 : bk.s1));
-    const int end0 = __ldg(a.col_ptr + (v0 ? j0 + 1 : bk.s1));
-    const int beg1 = __ldg(a.col_ptr + (v1 ? j1 : bk.s1));
-    const int end1 = __ldg(a.col_ptr + (v1 ? j1 + 1 : bk.s1));
-    double A0 = 0.0, w0 = 0.0, A1 = 0.0, w1 = 0.0;
-    int kd0 = 0, kd1 = 0;
-    if (v0) {
-      A0 = ld_stream_f64(a.A_in + j0, pol_first);
-      w0 = __ldg(a.w + j0);
-      kd0 = __ldg(a.kind + j0);
+    int beg[Q], end[Q], kd[Q];
+    double A[Q], w[Q], sum[Q];
+    const long long base = bk.s0 + pt * 32 * Q + lane;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const long long j = base + 32 * q;
+      const bool v = j < bk.s1;
+      beg[q] = __ldg(a.col_ptr + (v ? j : bk.s1));
+      end[q] = __ldg(a.col_ptr + (v ? j + 1 : bk.s1));
+      A[q] = 0.0;
+      w[q] = 0.0;
+      kd[q] = 0;
+      if (v) {
+        A[q] = ld_stream_f64(a.A_in + j, pol_first);
+        w[q] = __ldg(a.w + j);
+        kd[q] = __ldg(a.kind + j);
+      }
     }
-    if (v1) {
-      A1 = ld_stream_f64(a.A_in + j1, pol_first);
-      w1 = __ldg(a.w + j1);
-      kd1 = __ldg(a.kind + j1);
+    const int span_beg = __shfl_sync(kFull, beg[0], 0);
+    int span_end = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) span_end = max(span_end, __shfl_sync(kFull, end[q], 31));
+    warp_segments_sum_q<Q>(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g, pol_first, sum);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      asm volatile("" : "+r"(kd[q]), "+d"(w[q]) : : "memory");
+      const long long j = base + 32 * q;
+      if (j < bk.s1)
+        stream_update(a, j, beg[q], end[q], A[q], w[q], kd[q], sum[q], rho, trace_it, p_tda2, p_obj,
+                      pol_first, pol_last);
     }
-    const int span_beg = __shfl_sync(kFull, beg0, 0);
-    const int span_end = max(__shfl_sync(kFull, end0, 31), __shfl_sync(kFull, end1, 31));
-    double s0, s1;
-    warp_segments_sum2(a.row_idx, span_beg, span_end, beg0, end0, beg1, end1, sidx, lane, g,
-                       pol_first, s0, s1);
-    asm volatile("" : "+r"(kd0), "+d"(w0), "+r"(kd1), "+d"(w1) : : "memory");
-    if (v0) stream_update(a, j0, beg0, end0, A0, w0, kd0, s0, rho, trace_it, p_tda2, p_obj, pol_first, pol_last);
-    if (v1) stream_update(a, j1, beg1, end1, A1, w1, kd1, s1, rho, trace_it, p_tda2, p_obj, pol_first, pol_last);
   }
 }
 
-// kPairs: pair tiles (short routes) -- a separate instantiation, so the tile
-// form keeps its own register allocation.
-template <bool kPairs>
+// kQ: streams per lane (1: 32-stream tiles; 2 / 4: multi-route tiles for
+// short routes) -- separate instantiations, each with its own registers.
+template <int kQ>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
   __shared__ __align__(16) int sidx[kWarps][kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
@@ -544,8 +558,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   int* sb = sidx[threadIdx.x >> 5];
   const int sel = a.ctrl->v_sel;
   const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  if (kPairs)
-    stream_pass_pairs(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
+  if (kQ > 1)
+    stream_pass_multi<kQ>(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   else
     stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));

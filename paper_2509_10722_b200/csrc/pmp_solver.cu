@@ -429,10 +429,12 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    if (bk.pair_tiles)
-      k_stream_pass<true><<<h->grid1, kThreads, 0, s1>>>(a, bk);
+    if (bk.pair_tiles == 4)
+      k_stream_pass<4><<<h->grid1, kThreads, 0, s1>>>(a, bk);
+    else if (bk.pair_tiles == 2)
+      k_stream_pass<2><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else
-      k_stream_pass<false><<<h->grid1, kThreads, 0, s1>>>(a, bk);
+      k_stream_pass<1><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     mark(1);
     if (pipelined) {
       CK(cudaEventRecord(ev_k1[b], h->stream2));
@@ -843,11 +845,15 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     cb.col_idx = dalloc<int>(static_cast<size_t>(cb.nnz) + kIdxPad, b, h->stream);
     h->blocks.push_back(cb);
     build_csr(h, cb.s0, cb.s1, cb.row_ptr, cb.col_idx, nullptr);
-    // pair tiles for short routes: mean route length <= NUMPMP_PAIR_TILE_TAU (default 6)
+    // multi-route tiles for short routes: mean route length <= NUMPMP_PAIR_TILE_TAU
+    // (default 6) -> NUMPMP_TILE_Q (default 2) streams per lane
     double pair_tau = 6.0;
     if (const char* env = std::getenv("NUMPMP_PAIR_TILE_TAU")) pair_tau = std::atof(env);
+    int tile_q = 2;
+    if (const char* env = std::getenv("NUMPMP_TILE_Q")) tile_q = std::atoi(env) >= 4 ? 4 : 2;
     h->blocks.back().pair_tiles =
-        (cb.s1 > cb.s0 && static_cast<double>(cb.nnz) <= pair_tau * static_cast<double>(cb.s1 - cb.s0)) ? 1 : 0;
+        (cb.s1 > cb.s0 && static_cast<double>(cb.nnz) <= pair_tau * static_cast<double>(cb.s1 - cb.s0))
+            ? tile_q : 1;
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
     CK(cudaGetLastError());
     segment_block(h, h->blocks.back());
@@ -859,7 +865,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<false>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
   int occ3 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));

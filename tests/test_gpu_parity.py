@@ -771,11 +771,12 @@ def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restate
         assert ok, err
 
 
-@pytest.mark.parametrize("pair_tau", ["0", "100"])
-def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, restatement, oracle_mod, monkeypatch):
-    # the stream pass on 32-stream tiles and on 64-stream pair tiles (two
+@pytest.mark.parametrize("pair_tau,tile_q", [("0", "2"), ("100", "2"), ("100", "4")])
+def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, tile_q, restatement, oracle_mod, monkeypatch):
+    # the stream pass on 32-stream tiles and on multi-route tiles (2 or 4
     # routes per lane), forced; transit-like short routes and a ragged tail
     monkeypatch.setenv("NUMPMP_PAIR_TILE_TAU", pair_tau)
+    monkeypatch.setenv("NUMPMP_TILE_Q", tile_q)
     monkeypatch.setenv("NUMPMP_COL_BLOCKS", "2")
     p, _ = pmp.gen_transit(pmp.TransitSpec(12, 24, 5.0, 40, 30, 3, 6, 50.0, 2))
     cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=10.0)
