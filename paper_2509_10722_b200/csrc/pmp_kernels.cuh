@@ -171,7 +171,6 @@ struct BlockArgs {
   // streams): one lane per row, 32 consecutive rows per warp, no segment
   // metadata and no scan
   int row_mode;
-  int split;           // row_mode 2: lanes per row (1, 2 or 4)
   int pair_tiles;      // k_stream_pass streams per lane (1 = tiles; 2 / 4 for short routes)
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
@@ -803,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
     }
   };
-  if (kMode == 1) {
+  if (kMode != 0) {
     const long long ngroups = (bk.m + 31) / 32;
     for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
          g += (long long)gridDim.x * kWarps) {
@@ -813,75 +812,54 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       const int re = __ldg(bk.row_ptr + (valid ? r + 1 : bk.m));
       double Lprev = 0.0;
       if (!bk.first && valid) Lprev = __ldcg(a.Lacc + r);
-      const int span_beg = __shfl_sync(kFull, rb, 0);
-      const int span_end = __shfl_sync(kFull, re, 31);
-      const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
-                                         GatherX{src}, pol_first);
-      if (valid) row_done(r, bk.first ? s : Lprev + s);
-    }
-  } else if (kMode == 2) {
-    // Aligned rows (e.g. a time-expanded network: link (e, t+1) holds the
-    // streams of link (e, t) shifted by one departure, so entry u of R
-    // consecutive rows names R consecutive streams).  A warp takes R = 32/S
-    // consecutive rows, S lanes per row (lane = part * R + row): part p sums
-    // its near-equal share of the row, all lanes of a part in lockstep, so
-    // each step's gathers coalesce into a few sectors.  The S parts are then
-    // added in part order (fixed).  S trades coalescing for parallelism.
-    const int S = bk.split, R = 32 / S;
-    const int rr = lane % R, part = lane / R;
-    const long long ngroups = (bk.m + R - 1) / R;
-    const GatherX g{src};
-    for (long long gg = (long long)blockIdx.x * kWarps + wib; gg < ngroups;
-         gg += (long long)gridDim.x * kWarps) {
-      const long long r = gg * R + rr;
-      const bool valid = r < bk.m;
-      const int rb0 = __ldg(bk.row_ptr + (valid ? r : bk.m));
-      const int re0 = __ldg(bk.row_ptr + (valid ? r + 1 : bk.m));
-      const int n = re0 - rb0;
-      const int rb = rb0 + static_cast<int>((static_cast<long long>(part) * n) / S);
-      const int re = rb0 + static_cast<int>((static_cast<long long>(part + 1) * n) / S);
-      const int len = re - rb;
-      double Lprev = 0.0;
-      if (!bk.first && valid && part == 0) Lprev = __ldcg(a.Lacc + r);
-      int mx = len;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
       double s = 0.0;
-      for (int u0 = 0; u0 < mx; u0 += kUnroll) {
-        // the batch's indices: aligned 16-byte loads covering [rb + u0, rb +
-        // u0 + kUnroll) through L1, then a register select on the misalignment
-        int ii[kUnroll];
-        {
-          const int p0 = rb + u0;
-          const int q0 = p0 & ~3, off = p0 - q0;
-          int wv[kUnroll + 4];
+      if (kMode == 1) {
+        const int span_beg = __shfl_sync(kFull, rb, 0);
+        const int span_end = __shfl_sync(kFull, re, 31);
+        s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane, GatherX{src},
+                              pol_first);
+      } else {
+        // row_mode 2 (aligned rows, e.g. a time-expanded network: link (e, t+1)
+        // holds the streams of link (e, t) shifted by one departure, so entry u
+        // of 32 consecutive rows names 32 consecutive streams): lanes walk their
+        // own rows in lockstep, so each batch step's gathers coalesce into a
+        // couple of 128-byte lines; the row's indices come through L1 (each
+        // lane reads its row's sectors once).
+        int len = re - rb, mx = len;
 #pragma unroll
-          for (int t = 0; t < kUnroll / 4 + 1; ++t) {
-            int4 v4 = make_int4(0, 0, 0, 0);
-            if (u0 < len && q0 + 4 * t < re) v4 = __ldg(reinterpret_cast<const int4*>(bk.col_idx + q0) + t);
-            wv[4 * t] = v4.x;
-            wv[4 * t + 1] = v4.y;
-            wv[4 * t + 2] = v4.z;
-            wv[4 * t + 3] = v4.w;
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        const GatherX g{src};
+        for (int u0 = 0; u0 < mx; u0 += kUnroll) {
+          // the batch's indices: aligned 16-byte loads covering
+          // [rb + u0, rb + u0 + kUnroll) (each lane reads its own row's
+          // sectors, through L1), then a register select on the misalignment
+          int ii[kUnroll];
+          {
+            const int p0 = rb + u0;
+            const int q0 = p0 & ~3, off = p0 - q0;
+            int wv[kUnroll + 4];
+#pragma unroll
+            for (int t = 0; t < kUnroll / 4 + 1; ++t) {
+              int4 v4 = make_int4(0, 0, 0, 0);
+              if (u0 < len && q0 + 4 * t < re) v4 = __ldg(reinterpret_cast<const int4*>(bk.col_idx + q0) + t);
+              wv[4 * t] = v4.x;
+              wv[4 * t + 1] = v4.y;
+              wv[4 * t + 2] = v4.z;
+              wv[4 * t + 3] = v4.w;
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+              ii[u] = off == 0 ? wv[u] : (off == 1 ? wv[u + 1] : (off == 2 ? wv[u + 2] : wv[u + 3]));
           }
+          double vv[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) vv[u] = (u0 + u < len) ? g(ii[u]) : 0.0;
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u)
-            ii[u] = off == 0 ? wv[u] : (off == 1 ? wv[u + 1] : (off == 2 ? wv[u + 2] : wv[u + 3]));
+            if (u0 + u < len) s += vv[u];
         }
-        double vv[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) vv[u] = (u0 + u < len) ? g(ii[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (u0 + u < len) s += vv[u];
       }
-      // parts in order: part 0 receives sum of parts 1..S-1 added in order
-      double tot = s;
-      for (int p = 1; p < S; ++p) {
-        const double t = __shfl_sync(kFull, s, rr + p * R);
-        if (part == 0) tot += t;
-      }
-      if (valid && part == 0) row_done(r, bk.first ? tot : Lprev + tot);
+      if (valid) row_done(r, bk.first ? s : Lprev + s);
     }
   } else {
     const long long ustride = (long long)gridDim.x * kWarps;

@@ -176,7 +176,6 @@ struct ColBlock {
   int64_t nu = 0;
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
-  int split = 1;              // row_mode 2: lanes per row
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
 };
 
@@ -384,7 +383,6 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.index = b;
   k.first = b == 0;
   k.row_mode = cb.row_mode;
-  k.split = cb.split;
   k.pair_tiles = cb.pair_tiles;
   k.row_ptr = cb.row_ptr;
   k.m = h->m;
@@ -721,17 +719,7 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
       cudaFreeAsync(cnt, h->stream);
       aligned = 2 * c > static_cast<unsigned long long>(m);
     }
-    if (aligned) {
-      cb.row_mode = 2;
-      // lanes per row: enough warp items (rows / (32 / split)) for >= 4 waves of
-      // the persistent grid, whose size is not known yet: 148 SMs x 32 warps
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-      const int64_t slots = static_cast<int64_t>(sms) * 32;
-      cb.split = 1;
-      while (cb.split < 4 && m * cb.split / 32 < 4 * slots) cb.split *= 2;
-      if (const char* env = std::getenv("NUMPMP_ALIGNED_SPLIT")) cb.split = std::atoi(env) >= 4 ? 4 : (std::atoi(env) >= 2 ? 2 : 1);
-    }
+    if (aligned) cb.row_mode = 2;
   }
   int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
   int* row_vstart = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
@@ -916,8 +904,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
-    max_nu = std::max(max_nu, cb.row_mode == 2 ? (m * cb.split + 31) / 32
-                              : cb.row_mode == 1 ? (m + 31) / 32 : cb.nu);
+    max_nu = std::max(max_nu, cb.row_mode != 0 ? (m + 31) / 32 : cb.nu);
   }
   const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
   h->grid1 = static_cast<int>(std::max(

@@ -789,14 +789,13 @@ def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, tile_q, restate
         assert ok, err
 
 
-@pytest.mark.parametrize("aligned,split", [("0", "1"), ("1", "1"), ("1", "2"), ("1", "4")])
+@pytest.mark.parametrize("aligned", ["0", "1"])
 @pytest.mark.parametrize("shape", ["transit", "random"])
-def test_link_pass_aligned_rows_mode_matches_oracle(aligned, split, shape, restatement, oracle_mod, monkeypatch):
+def test_link_pass_aligned_rows_mode_matches_oracle(aligned, shape, restatement, oracle_mod, monkeypatch):
     # row_mode 2 (lanes walk consecutive rows in lockstep, indices through
-    # L1; 1, 2 or 4 lanes per row), forced on and off, on a time-expanded
-    # network (where it is chosen automatically) and on a random one
+    # L1), forced on and off, on a time-expanded network (where it is chosen
+    # automatically) and on a random one
     monkeypatch.setenv("NUMPMP_ALIGNED_ROWS", aligned)
-    monkeypatch.setenv("NUMPMP_ALIGNED_SPLIT", split)
     monkeypatch.setenv("NUMPMP_COL_BLOCKS", "2")
     if shape == "transit":
         p, _ = pmp.gen_transit(pmp.TransitSpec(12, 48, 5.0, 40, 30, 3, 48, 50.0, 2))
