@@ -61,7 +61,6 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
 constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
-static_assert(kUnroll % 4 == 0, "the aligned-rows link pass loads indices as int4");
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kMaxBlocks = 16;                 // max column blocks
 constexpr unsigned kFull = 0xffffffffu;
@@ -772,9 +771,7 @@ __device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
 // segment; a fixed-order segmented inclusive scan over the lanes leaves the
 // block partial of each row at its last ("tail") lane, which owns the row's
 // epilogue.  Rows never cross units, so no second combine pass exists.
-// kMode: 0 warp units, 1 row mode, 2 aligned rows (BlockArgs::row_mode);
-// one instantiation per mode so each keeps its own register allocation.
-template <int kPhase, int kMode>
+template <int kPhase>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
@@ -802,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
     }
   };
-  if (kMode != 0) {
+  if (bk.row_mode) {
     const long long ngroups = (bk.m + 31) / 32;
     for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
          g += (long long)gridDim.x * kWarps) {
@@ -813,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       double Lprev = 0.0;
       if (!bk.first && valid) Lprev = __ldcg(a.Lacc + r);
       double s = 0.0;
-      if (kMode == 1) {
+      if (bk.row_mode == 1) {
         const int span_beg = __shfl_sync(kFull, rb, 0);
         const int span_end = __shfl_sync(kFull, re, 31);
         s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane, GatherX{src},
@@ -830,28 +827,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
         for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
         const GatherX g{src};
         for (int u0 = 0; u0 < mx; u0 += kUnroll) {
-          // the batch's indices: aligned 16-byte loads covering
-          // [rb + u0, rb + u0 + kUnroll) (each lane reads its own row's
-          // sectors, through L1), then a register select on the misalignment
           int ii[kUnroll];
-          {
-            const int p0 = rb + u0;
-            const int q0 = p0 & ~3, off = p0 - q0;
-            int wv[kUnroll + 4];
-#pragma unroll
-            for (int t = 0; t < kUnroll / 4 + 1; ++t) {
-              int4 v4 = make_int4(0, 0, 0, 0);
-              if (u0 < len && q0 + 4 * t < re) v4 = __ldg(reinterpret_cast<const int4*>(bk.col_idx + q0) + t);
-              wv[4 * t] = v4.x;
-              wv[4 * t + 1] = v4.y;
-              wv[4 * t + 2] = v4.z;
-              wv[4 * t + 3] = v4.w;
-            }
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
-              ii[u] = off == 0 ? wv[u] : (off == 1 ? wv[u + 1] : (off == 2 ? wv[u + 2] : wv[u + 3]));
-          }
           double vv[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) ii[u] = (u0 + u < len) ? __ldg(bk.col_idx + rb + u0 + u) : 0;
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) vv[u] = (u0 + u < len) ? g(ii[u]) : 0.0;
 #pragma unroll

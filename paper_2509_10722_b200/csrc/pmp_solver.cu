@@ -404,17 +404,6 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
 // Launch order, work split and summation order are those of the serial
 // form, so results are bit-identical.  ev (serial form only, nullable):
 // events[0..launches] around every launch; ev[0] skipped unless record_first.
-template <int kPhase>
-void launch_link_pass(const numpmp_gpu* h, const IterArgs& a, const BlockArgs& bk, const double* src,
-                      double* out) {
-  if (bk.row_mode == 2)
-    k_link_pass<kPhase, 2><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
-  else if (bk.row_mode == 1)
-    k_link_pass<kPhase, 1><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
-  else
-    k_link_pass<kPhase, 0><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
-}
-
 void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, bool record_first,
                        bool pipelined = false) {
   IterArgs a = make_args(h, parity, mode);
@@ -452,13 +441,13 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
       CK(cudaStreamWaitEvent(h->stream, ev_k1[b], 0));
     }
     if (b + 1 < nb || acc_last)
-      launch_link_pass<LP_ACC>(h, a, bk, h->x, nullptr);
+      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else if (h->p2p)
-      launch_link_pass<LP_P2P>(h, a, bk, h->x, nullptr);
+      k_link_pass<LP_P2P><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else if (!h->sharded)
-      launch_link_pass<LP_FUSED>(h, a, bk, h->x, nullptr);
+      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     else
-      launch_link_pass<LP_GATHER>(h, a, bk, h->x, nullptr);
+      k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
     mark(2);
     if (pipelined) CK(cudaEventRecord(ev_k2[b], h->stream));
   }
@@ -585,9 +574,9 @@ void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
   IterArgs a = make_args(h, h->cur, MODE_AUX);
   for (int b = 0; b < h->nb(); ++b) {
     if (b + 1 < h->nb())
-      launch_link_pass<LP_ACC>(h, a, block_args(h, b), src, nullptr);
+      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, nullptr);
     else
-      launch_link_pass<LP_ROWSUM>(h, a, block_args(h, b), src, out);
+      k_link_pass<LP_ROWSUM><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, out);
     CK(cudaGetLastError());
   }
   if (h->p2p)
@@ -898,7 +887,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 0>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
   int occ3 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
   int64_t max_bs = 0, max_nu = 0;
