@@ -132,21 +132,6 @@ __global__ void k_seg_fill(const int* __restrict__ row_ptr, const int* __restric
     if (l == m - 1) vptr[v0 + ns] = b + d;
   }
 }
-// Aligned-rows test for the link pass's row_mode 2: counts the links l whose
-// row has the same length as row l+1 and whose first stream id is one less
-// (the shifted-departure structure of a time-expanded network).
-__global__ void k_aligned_rows(const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
-                               long long m, unsigned long long* __restrict__ count) {
-  unsigned long long c = 0;
-  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l + 1 < m;
-       l += (long long)gridDim.x * blockDim.x) {
-    const int b0 = row_ptr[l], e0 = row_ptr[l + 1], e1 = row_ptr[l + 2];
-    if (e0 > b0 && e1 - e0 == e0 - b0 && col_idx[e0] == col_idx[b0] + 1) ++c;
-  }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
-}
-
 __global__ void k_max_degree(const int* __restrict__ row_ptr, long long m, int* __restrict__ out) {
   int mx = 0;
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;

@@ -809,35 +809,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       const int re = __ldg(bk.row_ptr + (valid ? r + 1 : bk.m));
       double Lprev = 0.0;
       if (!bk.first && valid) Lprev = __ldcg(a.Lacc + r);
-      double s = 0.0;
-      if (bk.row_mode == 1) {
-        const int span_beg = __shfl_sync(kFull, rb, 0);
-        const int span_end = __shfl_sync(kFull, re, 31);
-        s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane, GatherX{src},
-                              pol_first);
-      } else {
-        // row_mode 2 (aligned rows, e.g. a time-expanded network: link (e, t+1)
-        // holds the streams of link (e, t) shifted by one departure, so entry u
-        // of 32 consecutive rows names 32 consecutive streams): lanes walk their
-        // own rows in lockstep, so each batch step's gathers coalesce into a
-        // couple of 128-byte lines; the row's indices come through L1 (each
-        // lane reads its row's sectors once).
-        int len = re - rb, mx = len;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
-        const GatherX g{src};
-        for (int u0 = 0; u0 < mx; u0 += kUnroll) {
-          int ii[kUnroll];
-          double vv[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) ii[u] = (u0 + u < len) ? __ldg(bk.col_idx + rb + u0 + u) : 0;
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) vv[u] = (u0 + u < len) ? g(ii[u]) : 0.0;
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u)
-            if (u0 + u < len) s += vv[u];
-        }
-      }
+      const int span_beg = __shfl_sync(kFull, rb, 0);
+      const int span_end = __shfl_sync(kFull, re, 31);
+      const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
+                                         GatherX{src}, pol_first);
       if (valid) row_done(r, bk.first ? s : Lprev + s);
     }
   } else {

@@ -689,27 +689,6 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   int row_mode_max = 64;
   if (const char* env = std::getenv("NUMPMP_ROW_MODE_MAX")) row_mode_max = std::atoi(env);
   cb.row_mode = maxd <= row_mode_max ? 1 : 0;
-  // Aligned rows (time-expanded networks): when most consecutive links carry
-  // the same streams shifted by one id, lanes walking consecutive rows in
-  // lockstep gather coalesced (row_mode 2).  NUMPMP_ALIGNED_ROWS: -1 auto
-  // (default: > 50% of the links), 0 never, 1 always.
-  {
-    int forced = -1;
-    if (const char* env = std::getenv("NUMPMP_ALIGNED_ROWS")) forced = std::atoi(env);
-    bool aligned = forced == 1;
-    if (forced < 0 && m > 1) {
-      unsigned long long* cnt = dalloc<unsigned long long>(1, &tmpb, h->stream);
-      CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), h->stream));
-      k_aligned_rows<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, cb.col_idx, m, cnt);
-      CK(cudaGetLastError());
-      unsigned long long c = 0;
-      CK(cudaMemcpyAsync(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
-      CK(cudaStreamSynchronize(h->stream));
-      cudaFreeAsync(cnt, h->stream);
-      aligned = 2 * c > static_cast<unsigned long long>(m);
-    }
-    if (aligned) cb.row_mode = 2;
-  }
   int* nseg = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
   int* row_vstart = dalloc<int>(static_cast<size_t>(m) + 1, &tmpb, h->stream);
   CK(cudaMemsetAsync(nseg + m, 0, sizeof(int), h->stream));
@@ -893,7 +872,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
-    max_nu = std::max(max_nu, cb.row_mode != 0 ? (m + 31) / 32 : cb.nu);
+    max_nu = std::max(max_nu, cb.row_mode ? (m + 31) / 32 : cb.nu);
   }
   const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
   h->grid1 = static_cast<int>(std::max(

@@ -787,25 +787,3 @@ def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, tile_q, restate
     for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw)]:
         ok, err = close(got, want)
         assert ok, err
-
-
-@pytest.mark.parametrize("aligned", ["0", "1"])
-@pytest.mark.parametrize("shape", ["transit", "random"])
-def test_link_pass_aligned_rows_mode_matches_oracle(aligned, shape, restatement, oracle_mod, monkeypatch):
-    # row_mode 2 (lanes walk consecutive rows in lockstep, indices through
-    # L1), forced on and off, on a time-expanded network (where it is chosen
-    # automatically) and on a random one
-    monkeypatch.setenv("NUMPMP_ALIGNED_ROWS", aligned)
-    monkeypatch.setenv("NUMPMP_COL_BLOCKS", "2")
-    if shape == "transit":
-        p, _ = pmp.gen_transit(pmp.TransitSpec(12, 48, 5.0, 40, 30, 3, 48, 50.0, 2))
-    else:
-        p = _gen(1500, 3000, 6.0, 2, True, 29)
-    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=10.0)
-    with pmp.PmpSolver(p, cfg) as s:
-        sol = s.solve()
-    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
-    assert sol.iterations == ref.iterations
-    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
-        ok, err = close(got, want)
-        assert ok, err
