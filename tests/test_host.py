@@ -247,3 +247,26 @@ def test_binary_reader_config_c_scale(tmp_path):
     np.testing.assert_array_equal(q.route_links, p.route_links)
     np.testing.assert_array_equal(q.stream_offsets, p.stream_offsets)
     print(f"read_problem config C: {dt:.2f} s")
+
+
+@pytest.mark.parametrize("m,world", [(1, 1), (10, 3), (1000000, 8), (182784, 8), (7, 8)])
+def test_link_owner_ranges_cover_the_links(m, world):
+    # the peer-memory exchange's owner partition (csrc/pmp_solver.cu
+    # create_impl: mo = ceil(m / world), rank q owns [q*mo, min(m, (q+1)*mo)))
+    from paper_2509_10722_b200.shard import link_owners
+
+    b = link_owners(m, world)
+    assert b[0] == 0 and b[-1] == m and len(b) == world + 1
+    assert np.all(np.diff(b) >= 0)
+    mo = -(-m // world)
+    for l in (0, m // 2, m - 1):  # owner(l) = l // mo lands in its range
+        q = l // mo
+        assert b[q] <= l < b[q + 1]
+
+
+def test_algorithmic_bytes_match_survey():
+    # B_alg = 8 nnz + 45 n + 76 m (+8) per iteration
+    import bench
+
+    k1, k2 = bench.alg_bytes(1000000, 10000000, 100006749)
+    assert k1 + k2 == 8 * 100006749 + 45 * 10000000 + 76 * 1000000 + 8
