@@ -143,17 +143,31 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# Test hooks for the multi-rank bench path on a one-GPU box (never set by
+# the driver): NUMPMP_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 and
+# NUMPMP_BENCH_BACKEND=gloo carries the plumbing collectives on CPU (NCCL
+# refuses two ranks on one GPU).  The ranks then time-share the GPU, so the
+# numbers measure nothing; the code path is what is exercised.
+BACKEND = os.environ.get("NUMPMP_BENCH_BACKEND", "nccl")
+
+
 def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("NUMPMP_BENCH_SAME_DEVICE") == "1":
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(BACKEND, init_method="env://")
     return rank, world, local
+
+
+def _coll_device():
+    return "cpu" if BACKEND == "gloo" else "cuda"
 
 
 def barrier_sync(world):
@@ -174,7 +188,7 @@ def max_over_ranks(world, value):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -185,7 +199,7 @@ def sum_over_ranks(world, value):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
