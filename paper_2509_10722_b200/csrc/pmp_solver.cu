@@ -902,10 +902,11 @@ void reset_ctrl(numpmp_gpu* h, double rho, int64_t iter) {
   c.rho_changed = 1;  // k_refresh_v builds v from B and price
   std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
   CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
-  if (!h->p2p) {  // v = B + price / rho of the uploaded state (the peer-memory path refreshes in-graph)
-    k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(make_args(h, h->cur, MODE_AUX));
-    CK(cudaGetLastError());
-  }
+  // v = B + price / rho of the new state, over all links (after set_cold /
+  // set_warm / set_state, B and price are complete on every rank of a
+  // sharded engine too)
+  k_refresh_v<<<h->grid3, kThreads, 0, h->stream>>>(make_args(h, h->cur, MODE_AUX));
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
 }
 

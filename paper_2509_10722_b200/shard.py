@@ -144,19 +144,31 @@ class ShardedPmpSolver:
         if rc:
             raise_for(rc, L.numpmp_gpu_last_error(self._h).decode())
 
-    def solve(self) -> Solution:
-        """Cold solve; x is this rank's shard, link vectors are global."""
+    def solve(self, warm=None) -> Solution:
+        """solve() / solve(WarmStart) (solver.hpp:411-413), collective over the
+        ranks.  warm.x0 is the GLOBAL start (each rank takes its shard), price
+        is global.  x of the result is this rank's shard; link vectors are
+        global and identical on every rank."""
         L = _lib.lib()
         p = self.local
         x, s, lam, lraw = np.empty(p.n), np.empty(p.m), np.empty(p.m), np.empty(p.m)
         info = _lib.SolutionInfo()
         cap = self._cfg.max_iters // self._cfg.trace_every + 2
         trace = (_lib.TraceRow * cap)()
-        for rc in (L.numpmp_gpu_set_cold(self._h),
-                   L.numpmp_gpu_run(self._h, _lib.ptr(x), _lib.ptr(s), _lib.ptr(lam), _lib.ptr(lraw),
-                                    C.byref(info), trace, cap)):
-            if rc:
-                raise_for(rc, L.numpmp_gpu_last_error(self._h).decode())
+        if warm is None:
+            rc = L.numpmp_gpu_set_cold(self._h)
+        else:
+            x0 = np.ascontiguousarray(np.asarray(warm.x0, np.float64)[self.stream_begin:self.stream_begin + p.n])
+            if x0.shape[0] != p.n:
+                raise ValueError("warm start: x0 length does not match n")
+            price = None if warm.price is None else np.ascontiguousarray(warm.price, np.float64)
+            rc = L.numpmp_gpu_set_warm(self._h, _lib.ptr(x0), _lib.ptr(price), float(warm.rho))
+        if rc:
+            raise_for(rc, L.numpmp_gpu_last_error(self._h).decode())
+        rc = L.numpmp_gpu_run(self._h, _lib.ptr(x), _lib.ptr(s), _lib.ptr(lam), _lib.ptr(lraw), C.byref(info),
+                              trace, cap)
+        if rc:
+            raise_for(rc, L.numpmp_gpu_last_error(self._h).decode())
         rows = [TraceRecord(trace[i].iter, trace[i].r_norm, trace[i].s_norm, trace[i].rho, trace[i].objective)
                 for i in range(min(info.trace_len, cap))]
         return Solution(x, s, lam, lraw, info.objective, SolveStatus(info.status), info.iterations,

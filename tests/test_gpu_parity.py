@@ -324,6 +324,34 @@ def test_p2p_exchange_ranks_match_oracle(world, blocks, restatement, oracle_mod,
     assert link_owners(p.m, world)[-1] == p.m
 
 
+def test_p2p_exchange_repeated_and_warm_solves(restatement, oracle_mod):
+    # the same ranks solving again (cold) and warm-started: each start state
+    # must rebuild v on every rank, whatever the previous solve left there
+    from paper_2509_10722_b200.shard import p2p_local_group, run_ranks
+
+    p = _gen(1200, 2400, 5.0, 2, True, 41)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    ranks = p2p_local_group(p, cfg, 2)
+    try:
+        first = run_ranks([s.solve for s in ranks])
+        again = run_ranks([s.solve for s in ranks])
+        x0 = np.concatenate([s.x for s in first])
+        warm = pmp.WarmStart(x0, first[0].lambda_raw, first[0].rho_final)
+        warm_sols = run_ranks([lambda s=s: s.solve(warm) for s in ranks])
+    finally:
+        for s in ranks:
+            s.close()
+    for sols in (first, again):
+        assert sols[0].iterations == ref.iterations
+        ok, err = close(np.concatenate([s.x for s in sols]), ref.x)
+        assert ok, err
+    wref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg), warm=(warm.x0, warm.price, warm.rho))
+    assert warm_sols[0].iterations == wref.iterations
+    ok, err = close(np.concatenate([s.x for s in warm_sols]), wref.x)
+    assert ok, err
+
+
 def test_p2p_exchange_is_deterministic(monkeypatch):
     # rank-order sums: identical bytes on a rerun, whatever the arrival order
     from paper_2509_10722_b200.shard import p2p_local_group, run_ranks
