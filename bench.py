@@ -473,6 +473,7 @@ def run_ours(args):
             "gen_s": t_gen,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": traffic,
+                         "frac_vs_8tbs_spec": achieved / 8000.0,
                          "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
                          "launch": "one pass over all column blocks per iteration",
                          "gather_bound": {"achieved_gathers_per_s": gather_rate, "peak_gathers_per_s": gather_peak,
