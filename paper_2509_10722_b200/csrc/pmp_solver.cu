@@ -875,10 +875,13 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     max_nu = std::max(max_nu, cb.row_mode ? (m + 31) / 32 : cb.nu);
   }
   const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
+  // grids: NUMPMP_GRID_MULT x the resident CTAs (1 = persistent)
+  long long gmult = 1;
+  if (const char* env = std::getenv("NUMPMP_GRID_MULT")) gmult = std::max(1, std::atoi(env));
   h->grid1 = static_cast<int>(std::max(
-      1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ1, 1))));
+      1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, gmult * sms * std::max(occ1, 1))));
   h->grid2 = static_cast<int>(std::max(
-      1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, 1LL * sms * std::max(occ2, 1))));
+      1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, gmult * sms * std::max(occ2, 1))));
   h->grid3 = static_cast<int>(std::max(
       1LL, std::min<long long>((m + kThreads - 1) / kThreads, 1LL * sms * std::max(occ3, 1))));
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
