@@ -69,6 +69,15 @@ typedef struct {
  * departures; streams arriving past the horizon are dropped (count in
  * *dropped).  Returns 0 or 5 (GenError). */
 int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, int64_t* dropped);
+/* TransitMetadata of a numpmp_gen_transit instance (transit.hpp:35-57):
+ * *n_ods usable OD pairs (TransitMetadata::ods, disconnected pairs skipped);
+ * per stream (length n) the OD index, route index and departure bin
+ * (TransitMetadata::streams); per OD its origin and destination station
+ * (length *n_ods).  Any pointer may be null; size with n_ods first.
+ * Returns 0, or 2 (ValidationError) for an instance not made by
+ * numpmp_gen_transit. */
+int numpmp_transit_meta(const numpmp_instance* inst, int64_t* n_ods, int32_t* od, int32_t* route,
+                        int32_t* t0, int32_t* od_origin, int32_t* od_dest);
 
 /* In-place capacity degradation with the reference's draw order. */
 int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor, uint64_t seed);
@@ -78,6 +87,11 @@ int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double facto
  * build_problem).  write_problem: encoding 0 auto (binary when m >= 1e6),
  * 1 text, 2 binary; the same bytes as the reference writer. */
 int numpmp_read_problem(const char* path, numpmp_instance** out);
+/* write_trace_csv (io.hpp:393-404): "iter,r_norm,s_norm,rho,objective" and
+ * one %.17g row per trace record, the same bytes as the reference.
+ * Returns 0 or 6 (IoError, the reference's message). */
+int numpmp_write_trace_csv(const char* path, int64_t rows, const int64_t* iter, const double* r_norm,
+                           const double* s_norm, const double* rho, const double* objective);
 int numpmp_write_problem(int64_t m, int64_t n, const double* capacities, const double* weights,
                          const uint8_t* kinds, const int64_t* offsets, const int32_t* routes,
                          const char* path, int encoding);

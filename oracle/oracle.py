@@ -243,6 +243,10 @@ class Reference:
         L.ref_gen_transit.argtypes = [C.c_int32, C.c_int32, D, I64, I64, C.c_int32, C.c_int32, D, C.c_uint64,
                                       C.POINTER(P), C.POINTER(I64)]
         L.ref_degrade.argtypes = [P, D, D, C.c_uint64, C.POINTER(P)]
+        L.ref_transit_meta.argtypes = [P, C.POINTER(I64), P, P, P, P, P]
+        L.ref_write_trace_csv.argtypes = [C.c_char_p, I64, P, P, P, P, P]
+        L.ref_transit_report.argtypes = [P, P, P, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(I64), P, P, P, P,
+                                         I64]
         L.ref_fail_and_prune.argtypes = [P, D, C.c_uint64, C.POINTER(P)]
         L.ref_prune_maps.argtypes = [P, P, P]
         L.ref_write_problem.argtypes = [P, C.c_char_p, C.c_int]
@@ -316,6 +320,12 @@ def _cfg_arrays(cfg: Config):
     return d, i
 
 
+def ref_write_trace_csv(ref: "Reference", path, it, r, s, rho, obj):
+    """io.hpp:393-404 through the reference."""
+    arrs = [np.ascontiguousarray(it, np.int64)] + [np.ascontiguousarray(a, np.float64) for a in (r, s, rho, obj)]
+    ref._err(ref.L.ref_write_trace_csv(os.fsencode(path), len(arrs[0]), *[_p(a) for a in arrs]))
+
+
 class RefProblem:
     def __init__(self, ref: Reference, h):
         self.ref = ref
@@ -343,6 +353,31 @@ class RefProblem:
     def write_problem(self, path, encoding="auto"):
         self.ref._err(self.ref.L.ref_write_problem(self.h, os.fsencode(path),
                                                    {"auto": 0, "text": 1, "binary": 2}[encoding]))
+
+    def transit_meta(self):
+        """(od, route, t0) per stream and (origin, dest) per OD (transit.hpp:35-57)."""
+        k = I64()
+        self.ref.L.ref_transit_meta(self.h, C.byref(k), None, None, None, None, None)
+        od, route, t0 = (np.empty(self.n, np.int32) for _ in range(3))
+        origin, dest = np.empty(k.value, np.int32), np.empty(k.value, np.int32)
+        self.ref.L.ref_transit_meta(self.h, C.byref(k), _p(od), _p(route), _p(t0), _p(origin), _p(dest))
+        return od, route, t0, origin, dest
+
+    def transit_report(self, x, lam, od, t0, csv_path):
+        """transit_report rows (stream ids, pi, lambda_hat per row) and the
+        reference CLI's CSV of them at csv_path."""
+        x = np.ascontiguousarray(x, np.float64)
+        lam = np.ascontiguousarray(lam, np.float64)
+        cap = self.nnz
+        nrows = I64()
+        stream, pi, hl = np.empty(self.n, np.int64), np.empty(self.n), np.empty(self.n, np.int64)
+        hats = np.empty(max(cap, 1))
+        self.ref._err(self.ref.L.ref_transit_report(self.h, _p(x), _p(lam), od, t0, os.fsencode(csv_path),
+                                                    C.byref(nrows), _p(stream), _p(pi), _p(hl), _p(hats), cap))
+        k = nrows.value
+        ends = np.cumsum(hl[:k])
+        rows = [hats[e - l:e] for e, l in zip(ends, hl[:k])]
+        return stream[:k], pi[:k], rows
 
     def degrade(self, p_degrade, factor, seed) -> "RefProblem":
         h = P()

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -473,6 +474,78 @@ double ref_prox_log(double z, double w, double rho, std::int64_t tau) {
 }
 double ref_prox_linear_nonneg(double z, double w, double rho, std::int64_t tau) {
   return prox_linear_nonneg_scalar(z, w, rho, tau);
+}
+
+// TransitMetadata::streams / ods (transit.hpp:35-57)
+int ref_transit_meta(void* h, std::int64_t* n_ods, std::int32_t* od, std::int32_t* route,
+                     std::int32_t* t0, std::int32_t* origin, std::int32_t* dest) {
+  const TransitMetadata& m = static_cast<RefProblem*>(h)->meta;
+  *n_ods = static_cast<std::int64_t>(m.ods.size());
+  for (std::size_t j = 0; j < m.streams.size(); ++j) {
+    if (od) od[j] = m.streams[j].od;
+    if (route) route[j] = m.streams[j].route;
+    if (t0) t0[j] = m.streams[j].t0;
+  }
+  for (std::size_t q = 0; q < m.ods.size(); ++q) {
+    if (origin) origin[q] = m.ods[q].origin;
+    if (dest) dest[q] = m.ods[q].dest;
+  }
+  return 0;
+}
+
+// io.hpp:393-404
+int ref_write_trace_csv(const char* path, std::int64_t rows, const std::int64_t* iter,
+                        const double* r, const double* s, const double* rho, const double* obj) {
+  try {
+    ConvergenceTrace t;
+    for (std::int64_t i = 0; i < rows; ++i) {
+      TraceRecord rec;
+      rec.iter = iter[i];
+      rec.r_norm = r[i];
+      rec.s_norm = s[i];
+      rec.rho = rho[i];
+      rec.objective = obj[i];
+      t.push_back(rec);
+    }
+    write_trace_csv(t, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// transit.hpp:340-374; the rows flattened (stream, pi, lambda_hat) and the
+// CSV the reference CLI writes for them (tools/numpmp.cpp:333-342 formatting)
+int ref_transit_report(void* h, const double* x, const double* lam, std::int32_t od, std::int32_t t0,
+                       const char* csv_path, std::int64_t* nrows, std::int64_t* stream, double* pi,
+                       std::int64_t* hat_len, double* hats, std::int64_t hat_cap) {
+  try {
+    RefProblem* r = static_cast<RefProblem*>(h);
+    std::vector<double> xv(x, x + r->p.n), lv(lam, lam + r->p.m);
+    auto rows = transit_report(r->p, xv, lv, r->meta, od, t0);
+    *nrows = static_cast<std::int64_t>(rows.size());
+    std::int64_t k = 0;
+    std::ofstream out(csv_path);
+    out << "stream,od,route,t0,x,pi,lambda_hat_path\n";
+    for (std::size_t i = 0; i < rows.size(); ++i) {
+      const auto& row = rows[i];
+      stream[i] = row.stream;
+      pi[i] = row.pi;
+      hat_len[i] = static_cast<std::int64_t>(row.lambda_hat.size());
+      for (double v : row.lambda_hat)
+        if (k < hat_cap) hats[k++] = v;
+      out << row.stream << ',' << row.od << ',' << row.route << ',' << row.t0 << ',' << row.x << ','
+          << row.pi << ',' << '"';
+      for (std::size_t q = 0; q < row.lambda_hat.size(); ++q) {
+        if (q) out << ' ';
+        out << row.lambda_hat[q];
+      }
+      out << '"' << '\n';
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
 }
 
 }  // extern "C"

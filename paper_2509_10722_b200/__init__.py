@@ -15,6 +15,7 @@ from .model import (
     Stream,
     StreamKind,
     TerminalLayout,
+    TransitMetadata,
     TransitSpec,
     WeightDist,
     build_problem,
@@ -43,11 +44,19 @@ from .solver import (
     to_string,
     update_rho,
 )
+from .transit import (
+    TransitReportRow,
+    normalized_route_prices,
+    transit_report,
+    write_trace_csv,
+    write_transit_report_csv,
+)
 
 __all__ = [
     "DeviceError", "DomainError", "GenError", "IoError", "SolverError", "ValidationError",
-    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitSpec", "WeightDist",
+    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitMetadata", "TransitSpec", "WeightDist",
     "build_problem", "degrade", "fail_and_prune", "PruneMap", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "read_problem", "validate", "write_problem",
     "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
     "check_termination", "objective", "recover_duals", "to_string", "update_rho",
+    "TransitReportRow", "normalized_route_prices", "transit_report", "write_trace_csv", "write_transit_report_csv",
 ]

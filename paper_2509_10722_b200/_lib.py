@@ -143,6 +143,8 @@ SIGNATURES = {
     "numpmp_degrade": (C.c_int, [I64, P, D, D, C.c_uint64]),
     "numpmp_fail_and_prune": (C.c_int, [I64, I64, P, P, P, P, P, D, C.c_uint64, C.POINTER(P), P, P]),
     "numpmp_read_problem": (C.c_int, [C.c_char_p, C.POINTER(P)]),
+    "numpmp_transit_meta": (C.c_int, [P, PI64, P, P, P, P, P]),
+    "numpmp_write_trace_csv": (C.c_int, [C.c_char_p, I64, P, P, P, P, P]),
     "numpmp_write_problem": (C.c_int, [I64, I64, P, P, P, P, P, C.c_char_p, C.c_int]),
     "numpmp_validate": (I64, [I64, I64, P, P, P, P, P, C.c_char_p, I64]),
     "numpmp_build_layout": (C.c_int, [I64, I64, P, P, P, P, P, P]),

@@ -365,6 +365,7 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
     std::vector<char> od_used(static_cast<std::size_t>(S) * S, 0);
     std::int64_t od_count = 0;
     std::vector<std::vector<std::vector<std::int32_t>>> od_routes;
+    std::vector<std::int32_t> od_o, od_d;
     guard = 0;
     while (od_count < spec->od_pairs) {
       const std::int32_t o = static_cast<std::int32_t>(rng.uniform_int(S));
@@ -388,15 +389,18 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
         routes.push_back(std::move(es));
       }
       od_routes.push_back(std::move(routes));
+      od_o.push_back(o);
+      od_d.push_back(d);
     }
     if (od_routes.empty()) return gen_error("transit spec: no usable OD pair");
     // one stream per (OD, route, departure) (transit.hpp:250-279)
     auto* inst = new numpmp_instance();
     inst->offsets.push_back(0);
     std::int64_t drop = 0;
-    for (const auto& routes : od_routes)
-      for (const auto& route : routes)
+    for (std::size_t odi = 0; odi < od_routes.size(); ++odi)
+      for (std::size_t r = 0; r < od_routes[odi].size(); ++r)
         for (std::int32_t dep = 0; dep < spec->departures_per_route; ++dep) {
+          const auto& route = od_routes[odi][r];
           const std::int32_t t0 =
               static_cast<std::int32_t>((std::int64_t(dep) * T) / spec->departures_per_route);
           if (t0 + std::int32_t(route.size()) - 1 > T - 1) {
@@ -409,6 +413,9 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
           inst->offsets.push_back(static_cast<std::int64_t>(inst->routes.size()));
           inst->kinds.push_back(0);
           inst->weights.push_back(1.0);
+          inst->t_od.push_back(static_cast<std::int32_t>(odi));
+          inst->t_route.push_back(static_cast<std::int32_t>(r));
+          inst->t_t0.push_back(t0);
         }
     if (inst->kinds.empty()) {
       delete inst;
@@ -417,6 +424,9 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
     inst->n = static_cast<std::int64_t>(inst->kinds.size());
     inst->m = std::int64_t(edges.size()) * T;
     inst->capacities.assign(static_cast<std::size_t>(inst->m), spec->seats);
+    inst->od_origin = std::move(od_o);
+    inst->od_dest = std::move(od_d);
+    inst->transit = true;
     if (dropped) *dropped = drop;
     *out = inst;
     return 0;
@@ -442,6 +452,24 @@ void numpmp_instance_export(const numpmp_instance* inst, double* capacities, dou
 }
 
 void numpmp_instance_free(numpmp_instance* inst) { delete inst; }
+
+int numpmp_transit_meta(const numpmp_instance* inst, int64_t* n_ods, int32_t* od, int32_t* route,
+                        int32_t* t0, int32_t* od_origin, int32_t* od_dest) {
+  if (!inst->transit) {
+    g_host_err = "transit metadata: not a transit instance";
+    return 2;
+  }
+  if (n_ods) *n_ods = static_cast<int64_t>(inst->od_origin.size());
+  auto put = [](const std::vector<std::int32_t>& v, int32_t* dst) {
+    if (dst) std::copy(v.begin(), v.end(), dst);
+  };
+  put(inst->t_od, od);
+  put(inst->t_route, route);
+  put(inst->t_t0, t0);
+  put(inst->od_origin, od_origin);
+  put(inst->od_dest, od_dest);
+  return 0;
+}
 
 int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor,
                    uint64_t seed) {

@@ -13,6 +13,10 @@ struct numpmp_instance {
   std::vector<std::uint8_t> kinds;
   std::vector<std::int64_t> offsets;
   std::vector<std::int32_t> routes;
+  // transit instances only (TransitMetadata, transit.hpp:41-57): per stream
+  // the OD index, route index and departure bin; per usable OD its stations
+  std::vector<std::int32_t> t_od, t_route, t_t0, od_origin, od_dest;
+  bool transit = false;
 };
 
 // Message of the last failing host call (numpmp_host_last_error), per thread.

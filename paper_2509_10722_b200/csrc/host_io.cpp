@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 #include <thread>
 #include <vector>
@@ -341,6 +342,29 @@ int numpmp_write_problem(int64_t m, int64_t n, const double* capacities, const d
   if (wrote != buf.size() || rc != 0) {
     g_host_err = std::string("write failed on '") + path + "'";
     return kIoError;
+  }
+  return 0;
+}
+
+int numpmp_write_trace_csv(const char* path, int64_t rows, const int64_t* iter, const double* r_norm,
+                           const double* s_norm, const double* rho, const double* objective) {
+  // io.hpp:393-404
+  const std::string p(path);
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_host_err = "cannot write '" + p + "'";
+    return 6;
+  }
+  std::string buf = "iter,r_norm,s_norm,rho,objective\n";
+  for (int64_t i = 0; i < rows; ++i) {
+    buf += std::to_string(iter[i]);
+    for (const double v : {r_norm[i], s_norm[i], rho[i], objective[i]}) buf += ',' + fmt_double(v);
+    buf += '\n';
+  }
+  const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+  if (std::fclose(f) != 0 || !ok) {
+    g_host_err = "write failed on '" + p + "'";
+    return 6;
   }
   return 0;
 }

@@ -236,8 +236,40 @@ class TransitSpec:  # transit.hpp:22-32
     seed: int = 0
 
 
-def gen_transit(spec: TransitSpec):
-    """transit.hpp:152-287 (bit-identical streams); returns (Problem, dropped)."""
+@dataclass
+class TransitMetadata:  # transit.hpp:41-57 (edges and warnings not carried)
+    stations: int
+    time_bins: int
+    bin_minutes: float
+    seats: float
+    od_origin: np.ndarray  # per usable OD (TransitMetadata::ods)
+    od_dest: np.ndarray
+    stream_od: np.ndarray  # per stream (TransitMetadata::streams)
+    stream_route: np.ndarray
+    stream_t0: np.ndarray
+    dropped_streams: int = 0
+
+    def link_id(self, edge: int, t: int) -> int:
+        return edge * self.time_bins + t
+
+
+def _transit_meta(inst, spec: "TransitSpec", n: int, dropped: int) -> TransitMetadata:
+    L = _lib.lib()
+    k = C.c_int64()
+    rc = L.numpmp_transit_meta(inst, C.byref(k), None, None, None, None, None)
+    if rc:
+        raise ValidationError(L.numpmp_host_last_error().decode())
+    od, route, t0 = (np.empty(n, np.int32) for _ in range(3))
+    origin, dest = np.empty(k.value, np.int32), np.empty(k.value, np.int32)
+    L.numpmp_transit_meta(inst, C.byref(k), _lib.ptr(od), _lib.ptr(route), _lib.ptr(t0), _lib.ptr(origin),
+                          _lib.ptr(dest))
+    return TransitMetadata(spec.stations, spec.time_bins, spec.bin_minutes, spec.seats, origin, dest, od, route, t0,
+                           dropped)
+
+
+def gen_transit(spec: TransitSpec, with_meta: bool = False):
+    """transit.hpp:152-287 (bit-identical streams); returns (Problem, dropped),
+    or (Problem, TransitMetadata) with with_meta=True (the reference's pair)."""
     L = _lib.lib()
     inst = C.c_void_p()
     dropped = C.c_int64()
@@ -246,6 +278,15 @@ def gen_transit(spec: TransitSpec):
     rc = L.numpmp_gen_transit(C.byref(cs), C.byref(inst), C.byref(dropped))
     if rc:
         raise GenError(L.numpmp_host_last_error().decode())
+    if with_meta:
+        m, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        L.numpmp_instance_sizes(inst, C.byref(m), C.byref(n), C.byref(nnz))
+        try:
+            meta = _transit_meta(inst, spec, n.value, dropped.value)
+        except BaseException:
+            L.numpmp_instance_free(inst)
+            raise
+        return _from_instance(inst), meta
     return _from_instance(inst), dropped.value
 
 

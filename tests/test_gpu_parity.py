@@ -733,6 +733,38 @@ def test_device_path_prices_bit_exact():
     np.testing.assert_array_equal(pi, want)
 
 
+
+def test_transit_report_from_device_solve(reference, tmp_path):
+    # solve on the device, path prices on the device, the
+    # report (transit.hpp:342-374) and both CSVs byte-identical to the
+    # reference's on the same solution
+    args = (12, 24, 5.0, 30, 40, 3, 24, 50.0, 4)
+    p, meta = pmp.gen_transit(pmp.TransitSpec(*args), with_meta=True)
+    rp = reference.gen_transit(*args)
+    with pmp.PmpSolver(p, pmp.SolverConfig(eps_abs=1e-5, rho0=1.0, max_iters=3000, trace_every=7)) as s:
+        sol = s.solve()
+        pi = s.path_prices(sol.lambda_)
+        n_rows = 0
+        for od in range(len(meta.od_origin)):
+            t0 = int(meta.stream_t0[meta.stream_od == od][0])
+            rows = pmp.transit_report(p, sol.x, sol.lambda_, meta, od, t0, solver=s)
+            assert [r.pi for r in rows] == [pi[r.stream] for r in rows]
+            stream, rpi, hats = rp.transit_report(sol.x, sol.lambda_, od, t0, str(tmp_path / "ref.csv"))
+            assert [r.stream for r in rows] == stream.tolist() and [r.pi for r in rows] == rpi.tolist()
+            assert [r.lambda_hat for r in rows] == [h.tolist() for h in hats]
+            pmp.write_transit_report_csv(rows, str(tmp_path / "mine.csv"))
+            assert (tmp_path / "mine.csv").read_bytes() == (tmp_path / "ref.csv").read_bytes()
+            n_rows += len(rows)
+    assert n_rows > 0 and sol.status == pmp.SolveStatus.Converged
+    from oracle.oracle import ref_write_trace_csv
+
+    pmp.write_trace_csv(sol.trace, str(tmp_path / "t_mine.csv"))
+    t = sol.trace
+    ref_write_trace_csv(reference, str(tmp_path / "t_ref.csv"), [r.iter for r in t], [r.r_norm for r in t],
+                        [r.s_norm for r in t], [r.rho for r in t], [r.objective for r in t])
+    assert (tmp_path / "t_mine.csv").read_bytes() == (tmp_path / "t_ref.csv").read_bytes()
+    assert len(t) > 2
+
 # ------------------------------------------- skew, ragged routes, edge shapes
 def _ragged_problem():
     # one stream over every link (a 700-link route spans several staging

@@ -270,3 +270,102 @@ def test_algorithmic_bytes_match_survey():
 
     k1, k2 = bench.alg_bytes(1000000, 10000000, 100006749)
     assert k1 + k2 == 8 * 100006749 + 45 * 10000000 + 76 * 1000000 + 8
+
+
+# ------------------------------------------------- reports
+TRANSIT_REPORT_CASES = [
+    (12, 24, 5.0, 30, 40, 3, 24, 50.0, 4),
+    (30, 48, 5.0, 80, 300, 5, 48, 20.0, 9),
+]
+
+
+@pytest.mark.parametrize("args", TRANSIT_REPORT_CASES)
+def test_transit_metadata_bit_exact(args, reference):
+    p, meta = pmp.gen_transit(pmp.TransitSpec(*args), with_meta=True)
+    od, route, t0, origin, dest = reference.gen_transit(*args).transit_meta()
+    np.testing.assert_array_equal(meta.stream_od, od)
+    np.testing.assert_array_equal(meta.stream_route, route)
+    np.testing.assert_array_equal(meta.stream_t0, t0)
+    np.testing.assert_array_equal(meta.od_origin, origin)
+    np.testing.assert_array_equal(meta.od_dest, dest)
+    assert meta.dropped_streams == pmp.gen_transit(pmp.TransitSpec(*args))[1]
+
+
+def test_transit_metadata_rejects_other_instances():
+    from paper_2509_10722_b200 import _lib
+
+    L = _lib.lib()
+    import ctypes as C
+
+    inst = C.c_void_p()
+    assert L.numpmp_gen_uncongested(C.byref(_spec(40, 20, 4.0, 2, ("constant", 1.0, 1.0), 9)._c()),
+                                    C.byref(inst)) == 0
+    k = C.c_int64()
+    assert L.numpmp_transit_meta(inst, C.byref(k), None, None, None, None, None) == 2
+    assert b"not a transit instance" in L.numpmp_host_last_error()
+    L.numpmp_instance_free(inst)
+
+
+@pytest.mark.parametrize("args", TRANSIT_REPORT_CASES)
+def test_transit_report_matches_reference(args, reference, tmp_path):
+    p, meta = pmp.gen_transit(pmp.TransitSpec(*args), with_meta=True)
+    rp = reference.gen_transit(*args)
+    rng = np.random.default_rng(5)
+    x = rng.random(p.n) * 3.0
+    lam = rng.random(p.m) * 0.2
+    lam[rng.random(p.m) < 0.4] = 0.0  # uncongested links price at zero
+    checked = 0
+    for od in range(len(meta.od_origin)):
+        for t0 in sorted(set(meta.stream_t0[meta.stream_od == od].tolist()))[:3]:
+            rows = pmp.transit_report(p, x, lam, meta, od, t0)
+            theirs = str(tmp_path / "ref.csv")
+            stream, pi, hats = rp.transit_report(x, lam, od, t0, theirs)
+            assert [r.stream for r in rows] == stream.tolist()
+            assert [r.pi for r in rows] == pi.tolist()  # bit-exact route-order sums
+            for r, h in zip(rows, hats):
+                assert r.lambda_hat == h.tolist()
+            mine = str(tmp_path / "mine.csv")
+            pmp.write_transit_report_csv(rows, mine)
+            assert open(mine, "rb").read() == open(theirs, "rb").read()
+            checked += len(rows)
+    assert checked > 0
+    # a departure bin with no stream: empty report, header only
+    assert pmp.transit_report(p, x, lam, meta, 0, -1) == []
+
+
+def test_transit_report_errors(reference, tmp_path):
+    args = TRANSIT_REPORT_CASES[0]
+    p, meta = pmp.gen_transit(pmp.TransitSpec(*args), with_meta=True)
+    k = len(meta.od_origin)
+    x, lam = np.ones(p.n), np.zeros(p.m)
+    with pytest.raises(pmp.ValidationError, match=rf"^unknown OD id {k}; available: 0\.\.{k - 1}$"):
+        pmp.transit_report(p, x, lam, meta, k, 0)
+    with pytest.raises(RuntimeError, match=rf"unknown OD id {k}; available: 0\.\.{k - 1}$"):
+        reference.gen_transit(*args).transit_report(x, lam, k, 0, str(tmp_path / "r.csv"))
+    with pytest.raises(pmp.ValidationError, match="metadata does not match problem"):
+        q = pmp.gen_uncongested(_spec(40, 20, 4.0, 2, ("constant", 1.0, 1.0), 9))
+        pmp.transit_report(q, np.ones(q.n), np.zeros(q.m), meta, 0, 0)
+    # all prices zero: normalized prices are 0 (transit.hpp:318-320)
+    rows = pmp.transit_report(p, x, lam, meta, 0, int(meta.stream_t0[meta.stream_od == 0][0]))
+    assert rows and all(v == 0.0 for r in rows for v in r.lambda_hat)
+
+
+def test_trace_csv_bytes_match_reference(reference, tmp_path):
+    from oracle.oracle import ref_write_trace_csv
+
+    rng = np.random.default_rng(3)
+    k = 40
+    it = np.cumsum(rng.integers(1, 20, k))
+    r, s = rng.random(k) * 1e-3, rng.random(k) ** 7
+    rho = 1000.0 * 2.0 ** rng.integers(-5, 5, k)
+    obj = -rng.random(k) * 1e6
+    r[3], s[4], obj[5], obj[6] = 0.0, 5e-324, -0.0, 1.0 / 3.0
+    trace = [pmp.TraceRecord(int(it[i]), r[i], s[i], rho[i], obj[i]) for i in range(k)]
+    mine, theirs = str(tmp_path / "mine.csv"), str(tmp_path / "ref.csv")
+    pmp.write_trace_csv(trace, mine)
+    ref_write_trace_csv(reference, theirs, it, r, s, rho, obj)
+    assert open(mine, "rb").read() == open(theirs, "rb").read()
+    pmp.write_trace_csv([], mine)
+    assert open(mine, "rb").read() == b"iter,r_norm,s_norm,rho,objective\n"
+    with pytest.raises(pmp.IoError, match=r"^cannot write '/nonexistent/dir/t\.csv'$"):
+        pmp.write_trace_csv(trace, "/nonexistent/dir/t.csv")
