@@ -46,6 +46,12 @@ CONFIGS = {
               desc="E: time-expanded transit, S=100 T=192 |E|=952, 9900 OD x 9 routes x 192 departures, seats 50"),
     # SURVEY.md 8(d) optional paper-shape cross-check (1847 s on an A100, tolerance and
     # iteration count unstated): more links than streams
+    # gen_congested (hot links on 10% of the streams each): the heavy-tailed
+    # streams-per-link distribution; hot rows are split over several warp units in the link pass
+    "F": dict(m=100000, n=1000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, congested=(0.001, 0.10),
+              desc="F: B-size congested, 100 hot links on ~10% of 1M streams each (mixed, w~U(0.5,1.5))"),
+    "G": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, congested=(0.001, 0.10),
+              desc="G: C congested, 1000 hot links on ~10% of 10M streams each (1.1e9 nonzeros)"),
     "P": dict(m=10000000, n=5000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
               desc="P: paper shape, 5M streams / 10M links, log, w=1"),
 }
@@ -68,8 +74,9 @@ def make_problem(name):
         p, _ = pmp.gen_transit(pmp.TransitSpec(*c["transit"]))
         return p
     w = pmp.WeightDist.uniform(0.5, 1.5) if c["uniform"] else pmp.WeightDist.constant(1.0)
-    p = pmp.gen_uncongested(pmp.GenSpec(m=c["m"], n=c["n"], avg_links_per_stream=c["avg"],
-                                        kind=pmp.GenKind(c["kind"]), weights=w, seed=c["seed"]))
+    spec = pmp.GenSpec(m=c["m"], n=c["n"], avg_links_per_stream=c["avg"], kind=pmp.GenKind(c["kind"]), weights=w,
+                       seed=c["seed"])
+    p = pmp.gen_congested(spec, *c["congested"]) if "congested" in c else pmp.gen_uncongested(spec)
     if "degrade" in c:
         p = pmp.degrade(p, *c["degrade"])
     return p

@@ -14,7 +14,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 OUT = os.path.join(LIB_DIR, "libnumpmp_cuda.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("pmp_solver.cu", "host_gen.cpp", "host_io.cpp")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pmp_kernels.cuh", "pmp_aux.cuh", "pmp_p2p.cuh",
-                                                            "host_instance.h")] + [
+                                                            "host_instance.h", "host_mt.h")] + [
     os.path.join(ROOT, "include", f) for f in ("numpmp_gpu.h", "numpmp_host.h")
 ]
 NVCC_FLAGS = [

@@ -17,17 +17,23 @@
 // no per-stream heap objects: generation of config C (10M streams, 100M
 // nonzeros) is bound by the sequential mt19937_64 stream only.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <iterator>
+#include <memory>
 #include <random>
+#include <stdexcept>
+#include <thread>
 #include <string>
 #include <unordered_set>
 #include <vector>
 
 #include "numpmp_host.h"
 #include "host_instance.h"
+#include "host_mt.h"
 
 thread_local std::string g_host_err;  // declared in host_instance.h
 
@@ -37,7 +43,11 @@ namespace {
 class Rng {
  public:
   explicit Rng(std::uint64_t seed) : eng_(seed) {}
-  std::uint64_t next_u64() { return eng_(); }
+  std::uint64_t next_u64() {
+    ++drawn;
+    return eng_();
+  }
+  std::uint64_t drawn = 0;  // raw outputs consumed (the jump-ahead offset)
   double uniform01() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
   double uniform(double a, double b) { return a + (b - a) * uniform01(); }
   bool bernoulli(double p) { return uniform01() < p; }
@@ -153,6 +163,187 @@ void draw(const numpmp_gen_spec* s, std::int64_t n, Rng& rng, numpmp_instance* i
   for (double& c : inst->capacities) c = rng.uniform(0.5, 1.5);
 }
 
+// gen.hpp:115-126 in parallel.  Pair (i, j) -- hot link i (ascending, as
+// sample_without_replacement sorts), stream j -- is decided by raw draw
+// P0 + i*n + j of the one sequential stream, so T threads each draw a
+// contiguous range of pairs from a jumped engine (host_mt.h) and keep the
+// selected pairs.  Each stream's final route is the sorted union of its
+// base route and its selected hot links: the same vector the reference's
+// skip-if-present sorted inserts build, in any insertion order.
+void hot_phase(std::uint64_t seed, std::uint64_t p0, const std::vector<std::int32_t>& hot, double p,
+               const numpmp_instance& base, numpmp_instance* inst) {
+  const std::int64_t n = base.n, H = static_cast<std::int64_t>(hot.size());
+  const std::uint64_t total = static_cast<std::uint64_t>(H) * static_cast<std::uint64_t>(n);
+  std::int64_t T = std::max(1u, std::thread::hardware_concurrency());
+  if (const char* env = std::getenv("NUMPMP_HOST_THREADS")) T = std::max(1, std::atoi(env));
+  T = std::max<std::int64_t>(1, std::min<std::int64_t>(T, static_cast<std::int64_t>(total >> 16) + 1));
+  // 1. draws: thread t owns pairs [a_t, a_{t+1}); hits are kept as stream
+  //    ids with the start of each hot link's run
+  struct Hits {
+    std::vector<std::int32_t> j;
+    std::vector<std::pair<std::int64_t, std::size_t>> runs;  // (hot index i, first position in j)
+  };
+  std::vector<Hits> hits(static_cast<std::size_t>(T));
+  const bool timing = std::getenv("NUMPMP_TIMING") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[numpmp] gen_congested %s: %.3f s\n", what,
+                 std::chrono::duration<double>(now - t_start).count());
+    t_start = now;
+  };
+  std::uint64_t w0[numpmp_mt::kN];
+  numpmp_mt::seed_window(seed, w0);
+  std::vector<int> ok(static_cast<std::size_t>(T), 1);
+  const std::uint64_t thr = static_cast<std::uint64_t>(std::ceil(std::ldexp(p, 53)));
+  auto draw_range = [&](std::int64_t t) {
+    const std::uint64_t a = total * static_cast<std::uint64_t>(t) / static_cast<std::uint64_t>(T);
+    const std::uint64_t b = total * static_cast<std::uint64_t>(t + 1) / static_cast<std::uint64_t>(T);
+    if (a == b) return;
+    std::uint64_t w[numpmp_mt::kN];
+    if (!numpmp_mt::jump(w0, p0 + a, w)) {
+      ok[static_cast<std::size_t>(t)] = 0;
+      return;
+    }
+    numpmp_mt::Engine eng(w);
+    Hits& h = hits[static_cast<std::size_t>(t)];
+    std::size_t cnt = 0;
+    h.j.resize(static_cast<std::size_t>(static_cast<double>(b - a) * p * 1.01) + 8192);
+    std::int64_t i = static_cast<std::int64_t>(a / static_cast<std::uint64_t>(n));
+    std::int64_t j = static_cast<std::int64_t>(a % static_cast<std::uint64_t>(n));
+    std::uint64_t d = a;
+    while (d < b) {
+      h.runs.emplace_back(i, cnt);
+      const std::int64_t jend = j + static_cast<std::int64_t>(
+                                        std::min<std::uint64_t>(b - d, static_cast<std::uint64_t>(n - j)));
+      d += static_cast<std::uint64_t>(jend - j);
+      while (j < jend) {  // branch-free: store every candidate, advance on a hit
+        const std::int64_t k1 = std::min<std::int64_t>(jend, j + 4096);
+        if (h.j.size() < cnt + 4096) h.j.resize(std::max(2 * h.j.size(), cnt + 4096));
+        std::int32_t* out = h.j.data();
+        for (; j < k1; ++j) {
+          out[cnt] = static_cast<std::int32_t>(j);
+          cnt += (eng() >> 11) < thr;  // Rng::bernoulli: k * 2^-53 < p  <=>  k < ceil(p * 2^53)
+        }
+      }
+      j = 0;
+      ++i;
+    }
+    h.j.resize(cnt);
+  };
+  {
+    std::vector<std::thread> th;
+    for (std::int64_t t = 1; t < T; ++t) th.emplace_back(draw_range, t);
+    draw_range(0);
+    for (auto& x : th) x.join();
+  }
+  for (int v : ok)
+    if (!v) throw std::runtime_error("gen_congested: mt19937_64 jump-ahead unavailable");
+  mark("draws");
+  // per hot link, the pieces (one per thread that drew part of its run)
+  struct Piece {
+    const std::int32_t* b;
+    const std::int32_t* e;
+  };
+  std::vector<std::vector<Piece>> pieces(static_cast<std::size_t>(H));
+  for (const Hits& h : hits)
+    for (std::size_t r = 0; r < h.runs.size(); ++r) {
+      const std::size_t e = r + 1 < h.runs.size() ? h.runs[r + 1].second : h.j.size();
+      pieces[static_cast<std::size_t>(h.runs[r].first)].push_back(
+          Piece{h.j.data() + h.runs[r].second, h.j.data() + e});
+    }
+  // 2. per stream range: hot links per stream (ascending), merged with the
+  //    base route
+  std::vector<std::vector<std::int32_t>> out(static_cast<std::size_t>(T));
+  std::vector<std::vector<std::int64_t>> lens(static_cast<std::size_t>(T));
+  auto build = [&](std::int64_t t) {
+    const std::int64_t ja = n * t / T, jb = n * (t + 1) / T;
+    // cursors into every (hot link, piece), advanced sub-block by sub-block
+    // (a sub-block's counts and hot links stay in cache)
+    std::vector<const std::int32_t*> cur, end;
+    std::vector<std::int32_t> cur_link;
+    for (std::int64_t i = 0; i < H; ++i)
+      for (const Piece& pc : pieces[static_cast<std::size_t>(i)]) {
+        cur.push_back(std::lower_bound(pc.b, pc.e, static_cast<std::int32_t>(ja)));
+        end.push_back(pc.e);
+        cur_link.push_back(hot[static_cast<std::size_t>(i)]);
+      }
+    auto& o = out[static_cast<std::size_t>(t)];
+    auto& ln = lens[static_cast<std::size_t>(t)];
+    ln.resize(static_cast<std::size_t>(jb - ja));
+    o.resize(static_cast<std::size_t>((base.offsets[jb] - base.offsets[ja]) +
+                                      static_cast<std::int64_t>(static_cast<double>(jb - ja) * p * H * 1.02)) +
+             4096);
+    std::size_t pos = 0;
+    constexpr std::int64_t kSub = 4096;
+    std::vector<std::int64_t> cnt(kSub + 1), fill(kSub);
+    std::vector<std::int32_t> add;
+    for (std::int64_t s0 = ja; s0 < jb; s0 += kSub) {
+      const std::int64_t s1 = std::min(jb, s0 + kSub);
+      std::fill(cnt.begin(), cnt.end(), 0);
+      for (std::size_t c = 0; c < cur.size(); ++c)
+        for (const std::int32_t* q = cur[c]; q < end[c] && *q < s1; ++q) ++cnt[static_cast<std::size_t>(*q - s0) + 1];
+      for (std::size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+      add.resize(static_cast<std::size_t>(cnt[static_cast<std::size_t>(s1 - s0)]));
+      std::copy(cnt.begin(), cnt.end() - 1, fill.begin());
+      for (std::size_t c = 0; c < cur.size(); ++c) {  // links ascending: each stream's list is sorted
+        const std::int32_t* q = cur[c];
+        for (; q < end[c] && *q < s1; ++q) add[static_cast<std::size_t>(fill[static_cast<std::size_t>(*q - s0)]++)] = cur_link[c];
+        cur[c] = q;
+      }
+      const std::size_t need = static_cast<std::size_t>(base.offsets[s1] - base.offsets[s0]) + add.size();
+      if (o.size() < pos + need) o.resize(std::max(2 * o.size(), pos + need));
+      for (std::int64_t j = s0; j < s1; ++j) {
+        const std::int32_t* rb = base.routes.data() + base.offsets[j];
+        const std::int32_t* re = base.routes.data() + base.offsets[j + 1];
+        const std::int32_t* hb = add.data() + cnt[static_cast<std::size_t>(j - s0)];
+        const std::int32_t* he = add.data() + cnt[static_cast<std::size_t>(j - s0) + 1];
+        std::int32_t* w = std::set_union(rb, re, hb, he, o.data() + pos);
+        const std::size_t len = static_cast<std::size_t>(w - (o.data() + pos));
+        ln[static_cast<std::size_t>(j - ja)] = static_cast<std::int64_t>(len);
+        pos += len;
+      }
+    }
+    o.resize(pos);
+  };
+  {
+    std::vector<std::thread> th;
+    for (std::int64_t t = 1; t < T; ++t) th.emplace_back(build, t);
+    build(0);
+    for (auto& x : th) x.join();
+  }
+  mark("per-stream union");
+  hits.clear();
+  hits.shrink_to_fit();
+  // 3. concatenate
+  inst->offsets.assign(static_cast<std::size_t>(n) + 1, 0);
+  std::vector<std::int64_t> start(static_cast<std::size_t>(T) + 1, 0);
+  for (std::int64_t t = 0; t < T; ++t) {
+    const std::int64_t ja = n * t / T;
+    std::int64_t acc = start[static_cast<std::size_t>(t)];
+    const auto& ln = lens[static_cast<std::size_t>(t)];
+    for (std::size_t k = 0; k < ln.size(); ++k) {
+      acc += ln[k];
+      inst->offsets[static_cast<std::size_t>(ja) + k + 1] = acc;
+    }
+    start[static_cast<std::size_t>(t) + 1] = acc;
+  }
+  inst->routes.resize(static_cast<std::size_t>(start[static_cast<std::size_t>(T)]));
+  {
+    std::vector<std::thread> th;
+    auto cp = [&](std::int64_t t) {
+      auto& o = out[static_cast<std::size_t>(t)];
+      std::copy(o.begin(), o.end(), inst->routes.begin() + start[static_cast<std::size_t>(t)]);
+      std::vector<std::int32_t>().swap(o);
+    };
+    for (std::int64_t t = 1; t < T; ++t) th.emplace_back(cp, t);
+    cp(0);
+    for (auto& x : th) x.join();
+  }
+  mark("concatenate");
+}
+
 }  // namespace
 
 extern "C" {
@@ -197,30 +388,14 @@ int numpmp_gen_congested(const numpmp_gen_spec* spec, double hot_link_fraction,
     const std::int64_t k = std::min(hot_count, spec->m);
     std::vector<std::int32_t> hot(static_cast<std::size_t>(k));
     rng.sample_without_replacement(spec->m, k, hot.data());
-    std::vector<std::vector<std::int32_t>> routes(static_cast<std::size_t>(n));
-    for (std::int64_t j = 0; j < n; ++j)
-      routes[static_cast<std::size_t>(j)].assign(base.routes.begin() + base.offsets[j],
-                                                 base.routes.begin() + base.offsets[j + 1]);
-    for (std::int32_t link : hot) {
-      for (auto& r : routes) {
-        if (!rng.bernoulli(hot_stream_fraction)) continue;
-        if (std::binary_search(r.begin(), r.end(), link)) continue;
-        r.insert(std::upper_bound(r.begin(), r.end(), link), link);
-      }
-    }
-    auto* inst = new numpmp_instance();
+    auto inst = std::make_unique<numpmp_instance>();
     inst->m = base.m;
     inst->n = base.n;
     inst->capacities = std::move(base.capacities);
     inst->weights = std::move(base.weights);
     inst->kinds = std::move(base.kinds);
-    inst->offsets.assign(static_cast<std::size_t>(n) + 1, 0);
-    for (std::int64_t j = 0; j < n; ++j) {
-      const auto& r = routes[static_cast<std::size_t>(j)];
-      inst->routes.insert(inst->routes.end(), r.begin(), r.end());
-      inst->offsets[static_cast<std::size_t>(j) + 1] = static_cast<std::int64_t>(inst->routes.size());
-    }
-    *out = inst;
+    hot_phase(spec->seed, rng.drawn, hot, hot_stream_fraction, base, inst.get());
+    *out = inst.release();
     return 0;
   } catch (const std::exception& e) {
     g_host_err = e.what();

@@ -173,6 +173,15 @@ struct BlockArgs {
   int pair_tiles;      // k_stream_pass streams per lane (1 = tiles; 2 / 4 for short routes)
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
+  // split rows (> 32 segments, e.g. the hot links of gen_congested): their
+  // segments carry vrow = row | 0x80000000 and span units ufirst..ulast
+  // (per unit; -1 elsewhere).  Each unit's piece goes to upart[u]; the piece
+  // that brings uctr[ufirst] to the row's unit count adds the pieces in unit
+  // order (deterministic whichever warp finishes last) and finishes the row.
+  const int* ufirst;
+  const int* ulast;
+  unsigned* uctr;
+  double* upart;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -850,8 +859,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       }
       const int next_row = __shfl_down_sync(kFull, row, 1);
       if (!valid || (lane != 31 && next_row == row)) continue;  // not the row's tail
-      const long long r = row;
-      row_done(r, bk.first ? s : __ldcg(a.Lacc + r) + s);
+      if (row >= 0) {
+        const long long r = row;
+        row_done(r, bk.first ? s : __ldcg(a.Lacc + r) + s);
+        continue;
+      }
+      // a piece of a split row
+      const long long r = row & 0x7fffffff;
+      const int uf = __ldg(bk.ufirst + u), ul = __ldg(bk.ulast + u);
+      __stcg(bk.upart + u, s);
+      __threadfence();
+      if (atomicAdd(bk.uctr + uf, 1u) != static_cast<unsigned>(ul - uf)) continue;
+      __threadfence();
+      double S = 0.0;
+      for (int k = uf; k <= ul; ++k) S += __ldcg(bk.upart + k);
+      bk.uctr[uf] = 0u;  // ready for the next launch
+      row_done(r, bk.first ? S : __ldcg(a.Lacc + r) + S);
     }
   }
   if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;

@@ -173,7 +173,11 @@ struct ColBlock {
   int* vptr = nullptr;        // nv+1: first CSR entry of each segment
   int* vrow = nullptr;        // nv: link of each segment
   int* uptr = nullptr;        // nu+1: first segment of each warp unit
-  int64_t nu = 0;
+  int* ufirst = nullptr;      // nu: first / last unit of the split row in the unit, or -1
+  int* ulast = nullptr;
+  unsigned* uctr = nullptr;   // nu: pieces of a split row done (at its first unit)
+  double* upart = nullptr;    // nu: a split row's partial load over the unit
+  int64_t nu = 0, split_rows = 0;
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
@@ -386,6 +390,10 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.pair_tiles = cb.pair_tiles;
   k.row_ptr = cb.row_ptr;
   k.m = h->m;
+  k.ufirst = cb.ufirst;
+  k.ulast = cb.ulast;
+  k.uctr = cb.uctr;
+  k.upart = cb.upart;
   return k;
 }
 
@@ -681,7 +689,9 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   CK(cudaMemcpyAsync(&maxd, dmax, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   cudaFreeAsync(dmax, h->stream);
-  cb.seg = std::max(kSeg, (maxd + 31) / 32);
+  // Segments of <= kSeg entries; a row of more than 32 segments (a hot link)
+  // is split over several warp units and combined in unit order.
+  cb.seg = kSeg;
   // Row mode when the longest row is short: a lane per row costs no
   // segment metadata or scan.  NUMPMP_ROW_MODE_MAX, default 64 entries
   // (C: -1.8%, P: -8%; B with 100-entry rows stays in units,
@@ -709,20 +719,49 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   cudaFreeAsync(nseg, h->stream);
   const int nv = vstart[static_cast<size_t>(m)];
   cb.nv = nv;
-  // greedy packing of whole rows into units of <= 32 segments
+  // greedy packing of whole rows into units of <= 32 segments; a row of
+  // more than 32 segments starts a unit and is cut every 32 segments (its
+  // last piece may share its unit with the following rows)
   std::vector<int> units;
   units.reserve(static_cast<size_t>(nv / 16 + 2));
+  std::vector<std::pair<int, int>> split;  // (first, last) unit of each split row
   int ubeg = 0;
   units.push_back(0);
   for (int64_t l = 0; l < m; ++l) {
-    const int re = vstart[static_cast<size_t>(l) + 1];
-    if (re - ubeg > 32) {
-      ubeg = vstart[static_cast<size_t>(l)];
+    const int rs = vstart[static_cast<size_t>(l)], re = vstart[static_cast<size_t>(l) + 1];
+    if (re - ubeg <= 32) continue;
+    if (rs > ubeg) {
+      ubeg = rs;
       units.push_back(ubeg);
+    }
+    if (re - rs > 32) {
+      const int uf = static_cast<int>(units.size()) - 1;
+      while (re - ubeg > 32) {
+        ubeg += 32;
+        units.push_back(ubeg);
+      }
+      split.emplace_back(uf, static_cast<int>(units.size()) - 1);
     }
   }
   units.push_back(nv);
   cb.nu = static_cast<int64_t>(units.size()) - 1;
+  cb.split_rows = static_cast<int64_t>(split.size());
+  if (!split.empty()) {
+    std::vector<int> uf(static_cast<size_t>(cb.nu), -1), ul(static_cast<size_t>(cb.nu), -1);
+    for (const auto& sr : split)
+      for (int u = sr.first; u <= sr.second; ++u) {
+        uf[static_cast<size_t>(u)] = sr.first;
+        ul[static_cast<size_t>(u)] = sr.second;
+      }
+    cb.ufirst = dalloc<int>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
+    cb.ulast = dalloc<int>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
+    cb.uctr = dalloc<unsigned>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
+    cb.upart = dalloc<double>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
+    CK(cudaMemcpyAsync(cb.ufirst, uf.data(), sizeof(int) * uf.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(cb.ulast, ul.data(), sizeof(int) * ul.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(cb.uctr, 0, sizeof(unsigned) * static_cast<size_t>(cb.nu), h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // uf / ul are host memory
+  }
   cb.uptr = dalloc<int>(units.size(), &h->dev_bytes, h->stream);
   CK(cudaMemcpyAsync(cb.uptr, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice,
                      h->stream));
@@ -1788,7 +1827,9 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   for (ColBlock& cb : h->blocks)
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
                     static_cast<void*>(cb.uptr), static_cast<void*>(cb.vptr),
-                    static_cast<void*>(cb.vrow)})
+                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.ufirst),
+                    static_cast<void*>(cb.ulast), static_cast<void*>(cb.uctr),
+                    static_cast<void*>(cb.upart)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {

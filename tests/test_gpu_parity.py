@@ -782,8 +782,8 @@ def _ragged_problem():
 
 
 SHAPE_CASES = {
-    # hot links: 10 links in ~10% of the streams each (rows of ~2000 entries,
-    # segment bound raised above 16 so a row still fits one warp unit)
+    # hot links: 10 links in ~10% of the streams each (rows of ~2000 entries:
+    # more than 32 segments, split over several warp units)
     "congested": lambda: pmp.gen_congested(pmp.GenSpec(m=2000, n=20000, avg_links_per_stream=4.0,
                                                        kind=pmp.GenKind.Mixed,
                                                        weights=pmp.WeightDist.uniform(0.5, 1.5), seed=13),
@@ -811,6 +811,47 @@ def test_skewed_and_ragged_shapes_match_oracle(shape, blocks, restatement, oracl
         ok, err = close(got, want)
         assert ok, err
     assert abs(sol.objective - ref.objective) <= RTOL * abs(ref.objective)
+
+
+def _hot_problem():
+    # hot rows of ~3000-6000 entries (split over 6-12 warp units) next to short rows
+    return pmp.gen_congested(pmp.GenSpec(m=3000, n=30000, avg_links_per_stream=5.0, kind=pmp.GenKind.Mixed,
+                                         weights=pmp.WeightDist.uniform(0.5, 1.5), seed=23), 0.004, 0.15)
+
+
+@pytest.mark.parametrize("blocks", [1, 2])
+def test_split_rows_deterministic_and_p2p(blocks, restatement, oracle_mod, monkeypatch):
+    # split rows combine their pieces in unit order: identical bytes on a
+    # rerun whatever warp finishes last, in the single-device engine and in
+    # the peer-memory sharded engine (LP_P2P)
+    from paper_2509_10722_b200.shard import p2p_local_group, run_ranks
+
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", str(blocks))
+    p = _hot_problem()
+    assert np.bincount(p.route_links, minlength=p.m).max() > 32 * 16 * blocks
+    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0, max_iters=20000)
+    with pmp.PmpSolver(p, cfg) as s:
+        a = s.solve()
+        b = s.solve()
+    assert a.iterations == b.iterations
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert a.iterations == ref.iterations
+    for got, want in [(a.x, ref.x), (a.lambda_raw, ref.lambda_raw)]:
+        ok, err = close(got, want)
+        assert ok, err
+    ranks = p2p_local_group(p, cfg, 2)
+    try:
+        sols = run_ranks([r.solve for r in ranks])
+        again = run_ranks([r.solve for r in ranks])
+    finally:
+        for r in ranks:
+            r.close()
+    assert sols[0].iterations == ref.iterations
+    ok, err = close(np.concatenate([q.x for q in sols]), ref.x)
+    assert ok, err
+    np.testing.assert_array_equal(np.concatenate([q.x for q in sols]), np.concatenate([q.x for q in again]))
 
 
 @pytest.mark.parametrize("row_mode_max", ["0", "100000"])

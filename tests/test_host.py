@@ -44,6 +44,25 @@ def test_config_b_nnz_matches_survey():
     assert p.nnz == 10002286
 
 
+@pytest.mark.parametrize("case,hot,threads", [
+    ((2000, 30000, 5.0, 2, ("uniform", 0.5, 1.5), 21), (0.01, 0.1), "7"),
+    ((2000, 30000, 5.0, 0, ("constant", 1.0, 1.0), 4), (0.02, 0.3), "1"),
+    ((300, 1000, 20.0, 1, ("constant", 1.0, 1.0), 8), (0.5, 0.9), "16"),   # hot links already on routes
+    ((50, 7, 3.0, 2, ("constant", 1.0, 1.0), 2), (1.0, 1.0), "3"),          # every link hot, every draw hits
+])
+def test_congested_generator_parallel_draws_bit_exact(case, hot, threads, reference, monkeypatch):
+    # the hot phase draws from jumped mt19937_64 engines on several threads
+    # (csrc/host_mt.h); ranges split hot links' runs at arbitrary streams
+    monkeypatch.setenv("NUMPMP_HOST_THREADS", threads)
+    ra = reference.gen(*case, congested=True, hot_link_fraction=hot[0], hot_stream_fraction=hot[1]).arrays()
+    p = pmp.gen_congested(_spec(*case), *hot)
+    assert p.nnz == ra.nnz
+    np.testing.assert_array_equal(p.stream_offsets, ra.stream_offsets)
+    np.testing.assert_array_equal(p.route_links, ra.route_links)
+    np.testing.assert_array_equal(p.weights, ra.weights)
+    np.testing.assert_array_equal(p.capacities, ra.capacities)
+
+
 def test_congested_generator_bit_exact(reference):
     case = (400, 300, 4.0, 2, ("uniform", 0.5, 1.5), 13)
     ra = reference.gen(*case, congested=True, hot_link_fraction=0.01, hot_stream_fraction=0.2).arrays()
