@@ -125,12 +125,9 @@ __global__ void k_seg_fill(const int* __restrict__ row_ptr, const int* __restric
        l += (long long)gridDim.x * blockDim.x) {
     const int b = row_ptr[l], d = row_ptr[l + 1] - b;
     const int v0 = row_vstart[l], ns = row_vstart[l + 1] - v0;
-    // rows of more than 32 segments are split over several warp units
-    // (k_link_pass): flagged in bit 31
-    const int tag = ns > 32 ? static_cast<int>(static_cast<unsigned>(l) | 0x80000000u) : static_cast<int>(l);
     for (int s = 0; s < ns; ++s) {
       vptr[v0 + s] = b + static_cast<int>((static_cast<long long>(s) * d) / ns);
-      vrow[v0 + s] = tag;
+      vrow[v0 + s] = static_cast<int>(l);
     }
     if (l == m - 1) vptr[v0 + ns] = b + d;
   }

@@ -62,6 +62,8 @@ constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the pas
 constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
+constexpr int kSplitMin = 32 * kSeg;           // rows longer than this are split into pieces
+constexpr int kPiece = 2 * kStageInts;         // entries per split-row piece
 constexpr int kMaxBlocks = 16;                 // max column blocks
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -162,7 +164,7 @@ struct BlockArgs {
   const int* col_idx;  // global stream ids, ascending per row
   const int* vptr;     // nv+1: first CSR entry of each segment
   const int* vrow;     // nv: link of each segment
-  const int* uptr;     // nu+1: first segment of each warp unit
+  const int2* units;   // nu: segment range [x, y) of each warp unit (whole rows)
   long long nv, nu;
   int index;           // block number b
   int first;           // b == 0
@@ -173,13 +175,15 @@ struct BlockArgs {
   int pair_tiles;      // k_stream_pass streams per lane (1 = tiles; 2 / 4 for short routes)
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
-  // split rows (> 32 segments, e.g. the hot links of gen_congested): their
-  // segments carry vrow = row | 0x80000000 and span units ufirst..ulast
-  // (per unit; -1 elsewhere).  Each unit's piece goes to upart[u]; the piece
-  // that brings uctr[ufirst] to the row's unit count adds the pieces in unit
-  // order (deterministic whichever warp finishes last) and finishes the row.
-  const int* ufirst;
-  const int* ulast;
+  // split rows (> kSplitMin entries, e.g. the hot links of gen_congested)
+  // are not in any unit: they are cut into pieces of <= kPiece entries,
+  // {entry begin, entry end, row, first slot of the row}, ordered by their
+  // relative position in the row so the warps in flight gather from a narrow
+  // window of x.  A piece's sum goes to upart[slot]; the piece that brings
+  // uctr[first slot] to the row's piece count adds the slots in order
+  // (deterministic whichever warp finishes last) and finishes the row.
+  const int4* pieces;
+  long long npieces;
   unsigned* uctr;
   double* upart;
 };
@@ -208,6 +212,23 @@ __device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
   double r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
   return r;
+}
+__device__ __forceinline__ int2 ld_nc_int2(const int2* p) {
+  int2 r;
+  asm("ld.global.nc.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_nc_int4(const int4* p) {
+  int4 r;
+  asm("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// Release of this thread's prior stores + acquire of the other pieces' (one
+// instruction instead of a fence and a relaxed atomic).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 __device__ __forceinline__ double ld_gather_f64(const double* p) {
   double r;
@@ -301,6 +322,52 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
         if (k + u < hi) acc += vv[u];
+    }
+    __syncwarp();
+    cb = nb;
+  }
+  return acc;
+}
+
+// Warp-cooperative gather-sum of one contiguous index range (a split-row
+// piece): rounds of kStageInts indices staged as in warp_segments_sum; lane
+// k gathers entries k, k+32, ... of each round, so one load instruction
+// covers 32 consecutive entries of the row (ascending stream ids: fewer
+// distinct lines per request than 32 separate segments).  Returns the
+// lane's partial; the caller reduces over the warp.
+template <class G>
+__device__ __forceinline__ double warp_strided_sum(const int* __restrict__ idx, int beg, int end,
+                                                   int* __restrict__ sidx, int lane, G g, uint64_t pol_stream) {
+  constexpr int NV = kStageInts / 128;
+  double acc = 0.0;
+  int cb = beg & ~3;
+  int4 buf[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int gp = cb + 4 * (lane + 32 * i);
+    if (gp < end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
+  }
+  while (cb < end) {
+    const int c1 = min(cb + kStageInts, end);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int o = 4 * (lane + 32 * i);
+      if (cb + o < c1) *reinterpret_cast<int4*>(sidx + o) = buf[i];
+    }
+    __syncwarp();
+    const int nb = cb + kStageInts;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int gp = nb + 4 * (lane + 32 * i);
+      if (gp < end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
+    }
+    for (int k = max(beg, cb) + lane; k < c1; k += 32 * kUnroll) {
+      double vv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + 32 * u < c1) ? g(sidx[k + 32 * u - cb]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (k + 32 * u < c1) acc += vv[u];
     }
     __syncwarp();
     cb = nb;
@@ -827,14 +894,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   } else {
     const long long ustride = (long long)gridDim.x * kWarps;
     long long u = (long long)blockIdx.x * kWarps + wib;
-    // this unit's segment range, loaded one unit ahead (the uptr -> vptr chain
-    // would otherwise put two dependent loads in front of every unit)
-    int v0 = 0, v1 = 0;
-    if (u < bk.nu) {
-      v0 = __ldg(bk.uptr + u);
-      v1 = __ldg(bk.uptr + u + 1);
-    }
+    // this unit's segment range, loaded one unit ahead (the units -> vptr
+    // chain would otherwise put two dependent loads in front of every unit)
+    int2 vr = make_int2(0, 0);
+    if (u < bk.nu) vr = ld_nc_int2(bk.units + u);
     for (; u < bk.nu; u += ustride) {
+      const int v0 = vr.x, v1 = vr.y;
       const int v = v0 + lane;
       const bool valid = v < v1;
       // independent loads, no select on a loaded value (it would hold the
@@ -843,10 +908,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       const int ve = __ldg(bk.vptr + (valid ? v + 1 : v1));
       int row = -1 - lane;
       if (valid) row = __ldg(bk.vrow + v);
-      if (u + ustride < bk.nu) {
-        v0 = __ldg(bk.uptr + u + ustride);
-        v1 = __ldg(bk.uptr + u + ustride + 1);
-      }
+      if (u + ustride < bk.nu) vr = ld_nc_int2(bk.units + u + ustride);
       const int span_beg = __shfl_sync(kFull, vb, 0);
       const int span_end = __shfl_sync(kFull, ve, 31);
       double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
@@ -859,22 +921,34 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       }
       const int next_row = __shfl_down_sync(kFull, row, 1);
       if (!valid || (lane != 31 && next_row == row)) continue;  // not the row's tail
-      if (row >= 0) {
-        const long long r = row;
-        row_done(r, bk.first ? s : __ldcg(a.Lacc + r) + s);
-        continue;
+      const long long r = row;
+      row_done(r, bk.first ? s : __ldcg(a.Lacc + r) + s);
+    }
+    // split rows, piece by piece
+    for (long long q = (long long)blockIdx.x * kWarps + wib; q < bk.npieces; q += ustride) {
+      const int4 pc = ld_nc_int4(bk.pieces + q);
+      double s = warp_strided_sum(bk.col_idx, pc.x, pc.y, sidx[wib], lane, GatherX{src}, pol_first);
+  #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);  // same bits on every lane
+      const int rb = __ldg(bk.row_ptr + pc.z), re = __ldg(bk.row_ptr + pc.z + 1);
+      const int np = (re - rb + kPiece - 1) / kPiece;
+      unsigned done = 0;
+      if (lane == 0) {
+        __stcg(bk.upart + pc.w + (pc.x - rb) / kPiece, s);
+        done = atom_add_acq_rel(bk.uctr + pc.w, 1u);
       }
-      // a piece of a split row
-      const long long r = row & 0x7fffffff;
-      const int uf = __ldg(bk.ufirst + u), ul = __ldg(bk.ulast + u);
-      __stcg(bk.upart + u, s);
-      __threadfence();
-      if (atomicAdd(bk.uctr + uf, 1u) != static_cast<unsigned>(ul - uf)) continue;
-      __threadfence();
+      done = __shfl_sync(kFull, done, 0);
+      if (done != static_cast<unsigned>(np - 1)) continue;
+      // last piece of the row: the slots in a fixed order (lane-strided, then butterfly)
       double S = 0.0;
-      for (int k = uf; k <= ul; ++k) S += __ldcg(bk.upart + k);
-      bk.uctr[uf] = 0u;  // ready for the next launch
-      row_done(r, bk.first ? S : __ldcg(a.Lacc + r) + S);
+      for (int k = lane; k < np; k += 32) S += __ldcg(bk.upart + pc.w + k);
+  #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(kFull, S, o);
+      if (lane == 0) {
+        bk.uctr[pc.w] = 0u;  // ready for the next launch
+        const long long r = pc.z;
+        row_done(r, bk.first ? S : __ldcg(a.Lacc + r) + S);
+      }
     }
   }
   if (kPhase == LP_ACC || kPhase == LP_ROWSUM) return;

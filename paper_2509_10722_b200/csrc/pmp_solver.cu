@@ -172,12 +172,11 @@ struct ColBlock {
   int* col_idx = nullptr;     // nnz + pad, global stream ids
   int* vptr = nullptr;        // nv+1: first CSR entry of each segment
   int* vrow = nullptr;        // nv: link of each segment
-  int* uptr = nullptr;        // nu+1: first segment of each warp unit
-  int* ufirst = nullptr;      // nu: first / last unit of the split row in the unit, or -1
-  int* ulast = nullptr;
-  unsigned* uctr = nullptr;   // nu: pieces of a split row done (at its first unit)
-  double* upart = nullptr;    // nu: a split row's partial load over the unit
-  int64_t nu = 0, split_rows = 0;
+  int2* units = nullptr;      // nu: segment range of each warp unit (whole rows)
+  int4* pieces = nullptr;     // npieces: split-row pieces (BlockArgs::pieces)
+  unsigned* uctr = nullptr;   // per split-row slot: pieces done (at the row's first slot)
+  double* upart = nullptr;    // per slot: a piece's partial load
+  int64_t nu = 0, npieces = 0;
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
@@ -381,7 +380,7 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.col_idx = cb.col_idx;
   k.vptr = cb.vptr;
   k.vrow = cb.vrow;
-  k.uptr = cb.uptr;
+  k.units = cb.units;
   k.nv = cb.nv;
   k.nu = cb.nu;
   k.index = b;
@@ -390,8 +389,8 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.pair_tiles = cb.pair_tiles;
   k.row_ptr = cb.row_ptr;
   k.m = h->m;
-  k.ufirst = cb.ufirst;
-  k.ulast = cb.ulast;
+  k.pieces = cb.pieces;
+  k.npieces = cb.npieces;
   k.uctr = cb.uctr;
   k.upart = cb.upart;
   return k;
@@ -719,52 +718,68 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   cudaFreeAsync(nseg, h->stream);
   const int nv = vstart[static_cast<size_t>(m)];
   cb.nv = nv;
-  // greedy packing of whole rows into units of <= 32 segments; a row of
-  // more than 32 segments starts a unit and is cut every 32 segments (its
-  // last piece may share its unit with the following rows)
-  std::vector<int> units;
+  // Greedy packing of whole rows into units of <= 32 segments.  Rows of
+  // more than kSplitMin entries (> 32 segments) are left out of the units:
+  // they become pieces of <= kPiece entries (BlockArgs::pieces), ordered by
+  // their relative position in the row, then by row.  Row mode has no
+  // units (a lane per row, any length).
+  std::vector<int> rp;
+  if (!cb.row_mode) {
+    rp.resize(static_cast<size_t>(m) + 1);
+    CK(cudaMemcpyAsync(rp.data(), cb.row_ptr, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  std::vector<int2> units;
   units.reserve(static_cast<size_t>(nv / 16 + 2));
-  std::vector<std::pair<int, int>> split;  // (first, last) unit of each split row
+  struct PieceKey {
+    double pos;
+    int4 pc;
+  };
+  std::vector<PieceKey> pieces;
+  int nslots = 0;
   int ubeg = 0;
-  units.push_back(0);
-  for (int64_t l = 0; l < m; ++l) {
+  auto close = [&](int end) {
+    if (end > ubeg) units.push_back(make_int2(ubeg, end));
+  };
+  for (int64_t l = 0; l < m && !cb.row_mode; ++l) {
     const int rs = vstart[static_cast<size_t>(l)], re = vstart[static_cast<size_t>(l) + 1];
-    if (re - ubeg <= 32) continue;
-    if (rs > ubeg) {
+    const int b = rp[static_cast<size_t>(l)], d = rp[static_cast<size_t>(l) + 1] - b;
+    if (d > kSplitMin) {
+      close(rs);
+      ubeg = re;  // the row's segments stay in vptr (contiguity) but in no unit
+      const int np = (d + kPiece - 1) / kPiece;
+      for (int k = 0; k < np; ++k)
+        pieces.push_back(PieceKey{(k + 0.5) / np,
+                                  make_int4(b + k * kPiece, b + std::min(d, (k + 1) * kPiece),
+                                            static_cast<int>(l), nslots)});
+      nslots += np;
+      continue;
+    }
+    if (re - ubeg > 32) {
+      close(rs);
       ubeg = rs;
-      units.push_back(ubeg);
-    }
-    if (re - rs > 32) {
-      const int uf = static_cast<int>(units.size()) - 1;
-      while (re - ubeg > 32) {
-        ubeg += 32;
-        units.push_back(ubeg);
-      }
-      split.emplace_back(uf, static_cast<int>(units.size()) - 1);
     }
   }
-  units.push_back(nv);
-  cb.nu = static_cast<int64_t>(units.size()) - 1;
-  cb.split_rows = static_cast<int64_t>(split.size());
-  if (!split.empty()) {
-    std::vector<int> uf(static_cast<size_t>(cb.nu), -1), ul(static_cast<size_t>(cb.nu), -1);
-    for (const auto& sr : split)
-      for (int u = sr.first; u <= sr.second; ++u) {
-        uf[static_cast<size_t>(u)] = sr.first;
-        ul[static_cast<size_t>(u)] = sr.second;
-      }
-    cb.ufirst = dalloc<int>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
-    cb.ulast = dalloc<int>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
-    cb.uctr = dalloc<unsigned>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
-    cb.upart = dalloc<double>(static_cast<size_t>(cb.nu), &h->dev_bytes, h->stream);
-    CK(cudaMemcpyAsync(cb.ufirst, uf.data(), sizeof(int) * uf.size(), cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemcpyAsync(cb.ulast, ul.data(), sizeof(int) * ul.size(), cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemsetAsync(cb.uctr, 0, sizeof(unsigned) * static_cast<size_t>(cb.nu), h->stream));
-    CK(cudaStreamSynchronize(h->stream));  // uf / ul are host memory
+  close(nv);
+  cb.nu = static_cast<int64_t>(units.size());
+  cb.npieces = static_cast<int64_t>(pieces.size());
+  if (!pieces.empty()) {
+    std::stable_sort(pieces.begin(), pieces.end(),
+                     [](const PieceKey& x, const PieceKey& y) { return x.pos < y.pos; });
+    std::vector<int4> pc(pieces.size());
+    for (size_t i = 0; i < pieces.size(); ++i) pc[i] = pieces[i].pc;
+    cb.pieces = dalloc<int4>(pc.size(), &h->dev_bytes, h->stream);
+    cb.uctr = dalloc<unsigned>(static_cast<size_t>(nslots), &h->dev_bytes, h->stream);
+    cb.upart = dalloc<double>(static_cast<size_t>(nslots), &h->dev_bytes, h->stream);
+    CK(cudaMemcpyAsync(cb.pieces, pc.data(), sizeof(int4) * pc.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(cb.uctr, 0, sizeof(unsigned) * static_cast<size_t>(nslots), h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // pc is host memory
   }
-  cb.uptr = dalloc<int>(units.size(), &h->dev_bytes, h->stream);
-  CK(cudaMemcpyAsync(cb.uptr, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice,
-                     h->stream));
+  if (!units.empty()) {
+    cb.units = dalloc<int2>(units.size(), &h->dev_bytes, h->stream);
+    CK(cudaMemcpyAsync(cb.units, units.data(), sizeof(int2) * units.size(), cudaMemcpyHostToDevice,
+                       h->stream));
+  }
   cb.vptr = dalloc<int>(static_cast<size_t>(nv) + 1, &h->dev_bytes, h->stream);
   cb.vrow = dalloc<int>(static_cast<size_t>(nv), &h->dev_bytes, h->stream);
   k_seg_fill<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, row_vstart, m, cb.vptr, cb.vrow);
@@ -911,7 +926,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
-    max_nu = std::max(max_nu, cb.row_mode ? (m + 31) / 32 : cb.nu);
+    max_nu = std::max(max_nu, cb.row_mode ? (m + 31) / 32 : cb.nu + cb.npieces);
   }
   const long long tiles1 = (max_bs + 31) / 32, tiles2 = max_nu;
   // grids: NUMPMP_GRID_MULT x the resident CTAs (1 = persistent)
@@ -1826,10 +1841,9 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   pt.mark("destroy: graphs + events");
   for (ColBlock& cb : h->blocks)
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
-                    static_cast<void*>(cb.uptr), static_cast<void*>(cb.vptr),
-                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.ufirst),
-                    static_cast<void*>(cb.ulast), static_cast<void*>(cb.uctr),
-                    static_cast<void*>(cb.upart)})
+                    static_cast<void*>(cb.units), static_cast<void*>(cb.vptr),
+                    static_cast<void*>(cb.vrow), static_cast<void*>(cb.pieces),
+                    static_cast<void*>(cb.uctr), static_cast<void*>(cb.upart)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {
