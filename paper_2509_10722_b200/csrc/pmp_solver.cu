@@ -177,6 +177,7 @@ struct ColBlock {
   unsigned* uctr = nullptr;   // per split-row slot: pieces done (at the row's first slot)
   double* upart = nullptr;    // per slot: a piece's partial load
   int64_t nu = 0, npieces = 0;
+  int piece = 0;              // entries per split-row piece
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
@@ -391,6 +392,7 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.m = h->m;
   k.pieces = cb.pieces;
   k.npieces = cb.npieces;
+  k.piece = cb.piece;
   k.uctr = cb.uctr;
   k.upart = cb.upart;
   return k;
@@ -737,6 +739,23 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   };
   std::vector<PieceKey> pieces;
   int nslots = 0;
+  // Piece size: fewer pieces (one release + ticket each) while keeping
+  // about 8 pieces per resident warp: kStageInts x [2, 16].
+  int64_t split_entries = 0;
+  for (int64_t l = 0; l < m && !cb.row_mode; ++l) {
+    const int d = rp[static_cast<size_t>(l) + 1] - rp[static_cast<size_t>(l)];
+    if (d > kSplitMin) split_entries += d;
+  }
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    const int64_t warps = static_cast<int64_t>(sms) * 2 * kWarps;
+    const int64_t rounds = split_entries / (8 * warps * kStageInts);
+    cb.piece = kStageInts * static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(16, rounds)));
+    if (const char* env = std::getenv("NUMPMP_PIECE_ROUNDS"))
+      cb.piece = kStageInts * std::max(1, std::atoi(env));
+  }
+  const int kPiece = cb.piece;
   int ubeg = 0;
   auto close = [&](int end) {
     if (end > ubeg) units.push_back(make_int2(ubeg, end));
