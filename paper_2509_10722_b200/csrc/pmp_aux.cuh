@@ -132,16 +132,6 @@ __global__ void k_seg_fill(const int* __restrict__ row_ptr, const int* __restric
     if (l == m - 1) vptr[v0 + ns] = b + d;
   }
 }
-// row_idx with the hot links' entries replaced by ~slot (slot_of[l] >= 0)
-__global__ void k_remap_hot(const int* __restrict__ row_idx, long long count, const int* __restrict__ slot_of,
-                            int* __restrict__ out) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int l = row_idx[t];
-    const int s = slot_of[l];
-    out[t] = s >= 0 ? ~s : l;
-  }
-}
 __global__ void k_max_degree(const int* __restrict__ row_ptr, long long m, int* __restrict__ out) {
   int mx = 0;
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m;

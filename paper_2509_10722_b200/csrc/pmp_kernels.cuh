@@ -64,7 +64,6 @@ constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kSplitMin = 32 * kSeg;           // rows longer than this are split into pieces
 constexpr int kMaxBlocks = 16;                 // max column blocks
-constexpr int kMaxHot = 2048;                  // hot links with v in shared memory (16 KB)
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { ST_RUNNING = -1, ST_CONVERGED = 0, ST_MAXITERS = 1, ST_TIMELIMIT = 2,
@@ -117,12 +116,6 @@ struct IterArgs {
   // stream side (CSC of R)
   const int* col_ptr;         // n+1
   const int* row_idx;         // nnz (+pad), link of each terminal in route order
-  // hot links (degree far above the mean, e.g. gen_congested's): row_idx
-  // with each hot link's entries replaced by ~slot, and the slot -> link
-  // table; the stream pass reads their v from shared memory
-  const int* row_idx_hot;
-  const int* hot_links;
-  int n_hot;
   const double* w;            // n
   const unsigned char* kind;  // n
   const int* deg;             // m, link degree (global)
@@ -276,11 +269,6 @@ __device__ __forceinline__ double prox_linear_nonneg(double z_sum, double w, dou
 struct GatherV {  // v_l (written by the previous link pass)
   const double* __restrict__ v;
   __device__ __forceinline__ double operator()(int l) const { return __ldg(v + l); }
-};
-struct GatherVHot {  // v_l, hot links (l = ~slot) from shared memory
-  const double* __restrict__ v;
-  const double* s;
-  __device__ __forceinline__ double operator()(int l) const { return l >= 0 ? __ldg(v + l) : s[~l]; }
 };
 struct GatherX {  // x_j (written by this iteration's stream pass)
   const double* __restrict__ x;
@@ -525,8 +513,7 @@ __global__ void __launch_bounds__(256) k_set_v(IterArgs a) {
 template <class G>
 __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockArgs& bk, G g,
                                                  double rho, bool trace_it, int* sidx,
-                                                 double& p_tda2, double& p_obj,
-                                                 const int* __restrict__ route_idx) {
+                                                 double& p_tda2, double& p_obj) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
@@ -549,7 +536,7 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
     }
     const int span_beg = __shfl_sync(kFull, beg, 0);
     const int span_end = __shfl_sync(kFull, end, 31);
-    const double sum = warp_segments_sum(route_idx, span_beg, span_end, beg, end, sidx, lane, g,
+    const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
                                          pol_first);
     // keep the kind test (and with it the wait for the kind / weight loads)
     // after the gather loop: the compiler otherwise hoists it and the warp
@@ -636,12 +623,9 @@ __device__ __forceinline__ void stream_pass_multi(const IterArgs& a, const Block
 
 // kQ: streams per lane (1: 32-stream tiles; 2 / 4: multi-route tiles for
 // short routes) -- separate instantiations, each with its own registers.
-// kHot: 32-stream tiles over row_idx_hot, the hot links' v staged in shared
-// memory once per CTA (same route-order sums, so the same bits).
-template <int kQ, bool kHot = false>
+template <int kQ>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
   __shared__ __align__(16) int sidx[kWarps][kStageInts];
-  __shared__ double s_vhot[kHot ? kMaxHot : 1];
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
   const long long k = a.ctrl->run_k + 1;
@@ -650,15 +634,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   int* sb = sidx[threadIdx.x >> 5];
   const int sel = a.ctrl->v_sel;
   const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  if (kHot) {
-    for (int i = threadIdx.x; i < a.n_hot; i += blockDim.x) s_vhot[i] = __ldg(v + __ldg(a.hot_links + i));
-    __syncthreads();
-    stream_pass_body(a, bk, GatherVHot{v, s_vhot}, rho, trace_it, sb, part[0], part[1], a.row_idx_hot);
-  } else if (kQ > 1) {
+  if (kQ > 1)
     stream_pass_multi<kQ>(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
-  } else {
-    stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1], a.row_idx);
-  }
+  else
+    stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 

@@ -215,9 +215,6 @@ struct numpmp_gpu {
   // problem
   int* col_ptr = nullptr;
   int* row_idx = nullptr;
-  int* row_idx_hot = nullptr;   // row_idx with hot links as ~slot (n_hot > 0)
-  int* hot_links = nullptr;     // n_hot: slot -> link
-  int n_hot = 0;
   double* w = nullptr;
   unsigned char* kind = nullptr;
   int* deg = nullptr;  // link degrees (global)
@@ -330,9 +327,6 @@ IterArgs make_args(numpmp_gpu* h, int parity, int mode) {
   IterArgs a{};
   a.col_ptr = h->col_ptr;
   a.row_idx = h->row_idx;
-  a.row_idx_hot = h->row_idx_hot;
-  a.hot_links = h->hot_links;
-  a.n_hot = h->n_hot;
   a.w = h->w;
   a.kind = h->kind;
   a.deg = h->deg;
@@ -444,9 +438,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    if (h->n_hot > 0)
-      k_stream_pass<1, true><<<h->grid1, kThreads, 0, s1>>>(a, bk);
-    else if (bk.pair_tiles == 4)
+    if (bk.pair_tiles == 4)
       k_stream_pass<4><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else if (bk.pair_tiles == 2)
       k_stream_pass<2><<<h->grid1, kThreads, 0, s1>>>(a, bk);
@@ -815,44 +807,6 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   cudaFreeAsync(row_vstart, h->stream);
 }
 
-// Hot links for the stream pass: degree >= 64x the mean (and >= 1024), the
-// top kMaxHot by degree, used when they hold >= 10% of the nonzeros (the
-// congested instances; none at A-E).  NUMPMP_HOT_LINKS=0 disables.
-void select_hot_links(numpmp_gpu* h) {
-  const int64_t m = h->m, nnz = h->nnz;
-  int cap = kMaxHot;
-  if (const char* env = std::getenv("NUMPMP_HOT_LINKS")) cap = std::min(kMaxHot, std::max(0, std::atoi(env)));
-  if (cap == 0 || nnz == 0 || m == 0) return;
-  std::vector<int> dg(static_cast<size_t>(m));
-  CK(cudaMemcpyAsync(dg.data(), h->deg, sizeof(int) * dg.size(), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  const double thr = std::max(1024.0, 64.0 * static_cast<double>(nnz) / static_cast<double>(m));
-  std::vector<int> cand;
-  for (int64_t l = 0; l < m; ++l)
-    if (dg[static_cast<size_t>(l)] >= thr) cand.push_back(static_cast<int>(l));
-  std::stable_sort(cand.begin(), cand.end(),
-                   [&](int x, int y) { return dg[static_cast<size_t>(x)] > dg[static_cast<size_t>(y)]; });
-  if (static_cast<int>(cand.size()) > cap) cand.resize(static_cast<size_t>(cap));
-  int64_t covered = 0;
-  for (int l : cand) covered += dg[static_cast<size_t>(l)];
-  if (cand.empty() || covered * 10 < nnz) return;
-  std::sort(cand.begin(), cand.end());
-  std::vector<int> slot(static_cast<size_t>(m), -1);
-  for (size_t i = 0; i < cand.size(); ++i) slot[static_cast<size_t>(cand[i])] = static_cast<int>(i);
-  int64_t tmpb = 0;
-  int* slot_d = dalloc<int>(static_cast<size_t>(m), &tmpb, h->stream);
-  h->hot_links = dalloc<int>(cand.size(), &h->dev_bytes, h->stream);
-  h->row_idx_hot = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &h->dev_bytes, h->stream);
-  CK(cudaMemcpyAsync(slot_d, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->hot_links, cand.data(), sizeof(int) * cand.size(), cudaMemcpyHostToDevice, h->stream));
-  k_remap_hot<<<grid_for(nnz), 256, 0, h->stream>>>(h->row_idx, nnz, slot_d, h->row_idx_hot);
-  CK(cudaGetLastError());
-  CK(cudaMemsetAsync(h->row_idx_hot + nnz, 0, sizeof(int) * kIdxPad, h->stream));
-  CK(cudaStreamSynchronize(h->stream));  // slot / cand are host memory
-  cudaFreeAsync(slot_d, h->stream);
-  h->n_hot = static_cast<int>(cand.size());
-}
-
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   PhaseTimer pt;
   CK(cudaSetDevice(h->device));
@@ -978,7 +932,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     segment_block(h, h->blocks.back());
   }
   CK(cudaStreamSynchronize(h->stream));
-  select_hot_links(h);
   pt.mark("create: device CSR build");
 
   // Persistent grids: resident blocks x SMs.
@@ -1885,7 +1838,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     cudaFree(h->xregion);
     h->v = h->v_alt[0] = h->v_alt[1] = nullptr;  // lived in the exchange region
   }
-  std::vector<void*> bufs = {h->row_idx_hot, h->hot_links, h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
+  std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
                              h->done_cnt, h->ep_part, h->k1_scalars, h->peer_tables,
                              h->v_alt[0], h->v_alt[1],

@@ -854,42 +854,6 @@ def test_split_rows_deterministic_and_p2p(blocks, restatement, oracle_mod, monke
     np.testing.assert_array_equal(np.concatenate([q.x for q in sols]), np.concatenate([q.x for q in again]))
 
 
-def test_hot_links_in_shared_memory_bit_identical(restatement, oracle_mod, monkeypatch):
-    # the stream pass reads the hot links' v from shared memory (route order
-    # unchanged): bit-identical to the plain pass, in one engine and in the
-    # peer-memory sharded engine (hot links chosen from each rank's shard)
-    from paper_2509_10722_b200.shard import p2p_local_group, run_ranks
-
-    p = pmp.gen_congested(pmp.GenSpec(m=3000, n=60000, avg_links_per_stream=3.0, kind=pmp.GenKind.Mixed,
-                                      weights=pmp.WeightDist.uniform(0.5, 1.5), seed=29), 0.004, 0.30)
-    deg = np.bincount(p.route_links, minlength=p.m)
-    assert deg.max() >= 64 * p.nnz / p.m
-    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0, max_iters=20000)
-    sols = {}
-    for hot in ("2048", "0"):
-        monkeypatch.setenv("NUMPMP_HOT_LINKS", hot)
-        with pmp.PmpSolver(p, cfg) as s:
-            sols[hot] = s.solve()
-    a, b = sols["2048"], sols["0"]
-    assert a.iterations == b.iterations
-    np.testing.assert_array_equal(a.x, b.x)
-    np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
-    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
-    assert a.iterations == ref.iterations
-    ok, err = close(a.x, ref.x)
-    assert ok, err
-    monkeypatch.setenv("NUMPMP_HOT_LINKS", "2048")
-    ranks = p2p_local_group(p, cfg, 2)
-    try:
-        got = run_ranks([r.solve for r in ranks])
-    finally:
-        for r in ranks:
-            r.close()
-    assert got[0].iterations == ref.iterations
-    ok, err = close(np.concatenate([q.x for q in got]), ref.x)
-    assert ok, err
-
-
 @pytest.mark.parametrize("row_mode_max", ["0", "100000"])
 @pytest.mark.parametrize("blocks", [1, 3])
 def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restatement, oracle_mod, monkeypatch):
