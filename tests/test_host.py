@@ -63,6 +63,17 @@ def test_congested_generator_parallel_draws_bit_exact(case, hot, threads, refere
     np.testing.assert_array_equal(p.capacities, ra.capacities)
 
 
+@pytest.mark.slow
+def test_congested_generator_config_f_bit_exact(reference):
+    # bench config F (1e8 hot-phase draws, 2e7 nonzeros): the jumped, threaded draws at scale
+    case = (100000, 1000000, 10.0, 2, ("uniform", 0.5, 1.5), 7)
+    ra = reference.gen(*case, congested=True, hot_link_fraction=0.001, hot_stream_fraction=0.1).arrays()
+    p = pmp.gen_congested(_spec(*case), 0.001, 0.1)
+    assert p.nnz == ra.nnz
+    np.testing.assert_array_equal(p.stream_offsets, ra.stream_offsets)
+    np.testing.assert_array_equal(p.route_links, ra.route_links)
+
+
 def test_congested_generator_bit_exact(reference):
     case = (400, 300, 4.0, 2, ("uniform", 0.5, 1.5), 13)
     ra = reference.gen(*case, congested=True, hot_link_fraction=0.01, hot_stream_fraction=0.2).arrays()
