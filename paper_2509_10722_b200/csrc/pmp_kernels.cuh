@@ -63,6 +63,10 @@ constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and ro
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kSplitMin = 32 * kSeg;           // rows longer than this are split into pieces
+#ifndef NUMPMP_PIECE_ROUNDS
+#define NUMPMP_PIECE_ROUNDS 8
+#endif
+constexpr int kPiece = NUMPMP_PIECE_ROUNDS * kStageInts;  // entries per split-row piece
 constexpr int kMaxBlocks = 16;                 // max column blocks
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -175,7 +179,7 @@ struct BlockArgs {
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
   // split rows (> kSplitMin entries, e.g. the hot links of gen_congested)
-  // are not in any unit: they are cut into pieces of <= `piece` entries,
+  // are not in any unit: they are cut into pieces of <= kPiece entries,
   // {entry begin, entry end, row, first slot of the row}, ordered by their
   // relative position in the row so the warps in flight gather from a narrow
   // window of x.  A piece's sum goes to upart[slot]; the piece that brings
@@ -183,7 +187,6 @@ struct BlockArgs {
   // (deterministic whichever warp finishes last) and finishes the row.
   const int4* pieces;
   long long npieces;
-  int piece;           // entries per piece (a multiple of kStageInts)
   unsigned* uctr;
   double* upart;
 };
@@ -223,11 +226,11 @@ __device__ __forceinline__ int4 ld_nc_int4(const int4* p) {
   asm("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
-// Release of this thread's prior stores (the finisher adds its own acquire
-// fence: only it reads the other pieces' partials).
-__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+// Release of this thread's prior stores + acquire of the other pieces' (one
+// instruction instead of a fence and a relaxed atomic).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
-  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
 __device__ __forceinline__ double ld_gather_f64(const double* p) {
@@ -847,7 +850,7 @@ __device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
 // segment; a fixed-order segmented inclusive scan over the lanes leaves the
 // block partial of each row at its last ("tail") lane, which owns the row's
 // epilogue.  Rows never cross units, so no second combine pass exists.
-template <int kPhase>
+template <int kPhase, bool kRowMode>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
@@ -875,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
     }
   };
-  if (bk.row_mode) {
+  if (kRowMode) {
     const long long ngroups = (bk.m + 31) / 32;
     for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
          g += (long long)gridDim.x * kWarps) {
@@ -931,15 +934,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
   #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);  // same bits on every lane
       const int rb = __ldg(bk.row_ptr + pc.z), re = __ldg(bk.row_ptr + pc.z + 1);
-      const int np = (re - rb + bk.piece - 1) / bk.piece;
+      const int np = (re - rb + kPiece - 1) / kPiece;
       unsigned done = 0;
       if (lane == 0) {
-        __stcg(bk.upart + pc.w + (pc.x - rb) / bk.piece, s);
-        done = atom_add_release(bk.uctr + pc.w, 1u);
+        __stcg(bk.upart + pc.w + (pc.x - rb) / kPiece, s);
+        done = atom_add_acq_rel(bk.uctr + pc.w, 1u);
       }
       done = __shfl_sync(kFull, done, 0);
       if (done != static_cast<unsigned>(np - 1)) continue;
-      __threadfence();  // acquire: the other pieces' partials (read with ld.cg below)
       // last piece of the row: the slots in a fixed order (lane-strided, then butterfly)
       double S = 0.0;
       for (int k = lane; k < np; k += 32) S += __ldcg(bk.upart + pc.w + k);

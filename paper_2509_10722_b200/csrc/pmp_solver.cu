@@ -177,7 +177,6 @@ struct ColBlock {
   unsigned* uctr = nullptr;   // per split-row slot: pieces done (at the row's first slot)
   double* upart = nullptr;    // per slot: a piece's partial load
   int64_t nu = 0, npieces = 0;
-  int piece = 0;              // entries per split-row piece
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
@@ -392,11 +391,22 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.m = h->m;
   k.pieces = cb.pieces;
   k.npieces = cb.npieces;
-  k.piece = cb.piece;
   k.uctr = cb.uctr;
   k.upart = cb.upart;
   return k;
 }
+
+// The link pass of one column block: row mode and warp units (+ split-row
+// pieces) are separate instantiations, so neither form's code shapes the
+// other's register allocation.
+template <int kPhase>
+void launch_link_pass(const numpmp_gpu* h, const IterArgs& a, const BlockArgs& bk, const double* src, double* out) {
+  if (bk.row_mode)
+    k_link_pass<kPhase, true><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
+  else
+    k_link_pass<kPhase, false><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
+}
+
 
 // One PMP iteration on the stream: for each column block b the stream pass
 // K1(b) and the link-pass gather K2(b); the last block's link pass is fused
@@ -450,13 +460,13 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
       CK(cudaStreamWaitEvent(h->stream, ev_k1[b], 0));
     }
     if (b + 1 < nb || acc_last)
-      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+      launch_link_pass<LP_ACC>(h, a, bk, h->x, nullptr);
     else if (h->p2p)
-      k_link_pass<LP_P2P><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+      launch_link_pass<LP_P2P>(h, a, bk, h->x, nullptr);
     else if (!h->sharded)
-      k_link_pass<LP_FUSED><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+      launch_link_pass<LP_FUSED>(h, a, bk, h->x, nullptr);
     else
-      k_link_pass<LP_GATHER><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, h->x, nullptr);
+      launch_link_pass<LP_GATHER>(h, a, bk, h->x, nullptr);
     mark(2);
     if (pipelined) CK(cudaEventRecord(ev_k2[b], h->stream));
   }
@@ -583,9 +593,9 @@ void global_row_sums(numpmp_gpu* h, const double* src, double* out) {
   IterArgs a = make_args(h, h->cur, MODE_AUX);
   for (int b = 0; b < h->nb(); ++b) {
     if (b + 1 < h->nb())
-      k_link_pass<LP_ACC><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, nullptr);
+      launch_link_pass<LP_ACC>(h, a, block_args(h, b), src, nullptr);
     else
-      k_link_pass<LP_ROWSUM><<<h->grid2, kThreads, 0, h->stream>>>(a, block_args(h, b), src, out);
+      launch_link_pass<LP_ROWSUM>(h, a, block_args(h, b), src, out);
     CK(cudaGetLastError());
   }
   if (h->p2p)
@@ -739,23 +749,6 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   };
   std::vector<PieceKey> pieces;
   int nslots = 0;
-  // Piece size: fewer pieces (one release + ticket each) while keeping
-  // about 8 pieces per resident warp: kStageInts x [2, 16].
-  int64_t split_entries = 0;
-  for (int64_t l = 0; l < m && !cb.row_mode; ++l) {
-    const int d = rp[static_cast<size_t>(l) + 1] - rp[static_cast<size_t>(l)];
-    if (d > kSplitMin) split_entries += d;
-  }
-  {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-    const int64_t warps = static_cast<int64_t>(sms) * 2 * kWarps;
-    const int64_t rounds = split_entries / (8 * warps * kStageInts);
-    cb.piece = kStageInts * static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(16, rounds)));
-    if (const char* env = std::getenv("NUMPMP_PIECE_ROUNDS"))
-      cb.piece = kStageInts * std::max(1, std::atoi(env));
-  }
-  const int kPiece = cb.piece;
   int ubeg = 0;
   auto close = [&](int end) {
     if (end > ubeg) units.push_back(make_int2(ubeg, end));
@@ -939,7 +932,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, false>, kThreads, 0));
   int occ3 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
   int64_t max_bs = 0, max_nu = 0;
