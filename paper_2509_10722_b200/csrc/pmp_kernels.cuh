@@ -1008,7 +1008,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
 // kSrc 1 = one device, on the loads the last block accumulated into Lacc.
 // Residual partials, last-CTA finalize.
 template <int kSrc>
-__global__ void __launch_bounds__(kThreads) k_link_epilogue(IterArgs a) {
+#ifndef NUMPMP_EPI_MINB
+#define NUMPMP_EPI_MINB 4  // 4 CTAs per SM (64 registers): C -0.35% (profiles/r1_congested_sweeps.txt, lib A/B)
+#endif
+__global__ void __launch_bounds__(kThreads, NUMPMP_EPI_MINB) k_link_epilogue(IterArgs a) {
   __shared__ bool s_last;
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
