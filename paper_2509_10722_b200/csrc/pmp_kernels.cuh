@@ -850,7 +850,9 @@ __device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
 // segment; a fixed-order segmented inclusive scan over the lanes leaves the
 // block partial of each row at its last ("tail") lane, which owns the row's
 // epilogue.  Rows never cross units, so no second combine pass exists.
-template <int kPhase, bool kRowMode>
+// kForm: 0 row mode, 1 warp units, 2 warp units + split-row pieces (separate
+// instantiations: neither form's code shapes another's register allocation).
+template <int kPhase, int kForm>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
@@ -878,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       link_epilogue(a, r, L, __ldg(a.deg + r), rho, part, pol_first, pol_last);
     }
   };
-  if (kRowMode) {
+  if (kForm == 0) {
     const long long ngroups = (bk.m + 31) / 32;
     for (long long g = (long long)blockIdx.x * kWarps + wib; g < ngroups;
          g += (long long)gridDim.x * kWarps) {
@@ -928,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, 
       row_done(r, bk.first ? s : __ldcg(a.Lacc + r) + s);
     }
     // split rows, piece by piece
-    for (long long q = (long long)blockIdx.x * kWarps + wib; q < bk.npieces; q += ustride) {
+    for (long long q = (long long)blockIdx.x * kWarps + wib; kForm == 2 && q < bk.npieces; q += ustride) {
       const int4 pc = ld_nc_int4(bk.pieces + q);
       double s = warp_strided_sum(bk.col_idx, pc.x, pc.y, sidx[wib], lane, GatherX{src}, pol_first);
   #pragma unroll

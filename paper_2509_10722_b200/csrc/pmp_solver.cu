@@ -396,15 +396,16 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   return k;
 }
 
-// The link pass of one column block: row mode and warp units (+ split-row
-// pieces) are separate instantiations, so neither form's code shapes the
-// other's register allocation.
+// The link pass of one column block in its form: row mode, warp units, or
+// warp units + split-row pieces (k_link_pass kForm 0 / 1 / 2).
 template <int kPhase>
 void launch_link_pass(const numpmp_gpu* h, const IterArgs& a, const BlockArgs& bk, const double* src, double* out) {
   if (bk.row_mode)
-    k_link_pass<kPhase, true><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
+    k_link_pass<kPhase, 0><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
+  else if (bk.npieces == 0)
+    k_link_pass<kPhase, 1><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
   else
-    k_link_pass<kPhase, false><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
+    k_link_pass<kPhase, 2><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
 }
 
 
@@ -932,7 +933,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, false>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 2>, kThreads, 0));
   int occ3 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
   int64_t max_bs = 0, max_nu = 0;
