@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <iterator>
 #include <memory>
 #include <random>
@@ -163,6 +164,27 @@ void draw(const numpmp_gen_spec* s, std::int64_t n, Rng& rng, numpmp_instance* i
   for (double& c : inst->capacities) c = rng.uniform(0.5, 1.5);
 }
 
+// fn(t) for t in [0, T) on T threads (t = 0 on the caller's); the first
+// exception is rethrown after the join (inside a std::thread it would
+// terminate the process).
+template <class F>
+void run_threads(std::int64_t T, F fn) {
+  std::vector<std::exception_ptr> err(static_cast<std::size_t>(T));
+  auto guarded = [&](std::int64_t t) {
+    try {
+      fn(t);
+    } catch (...) {
+      err[static_cast<std::size_t>(t)] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> th;
+  for (std::int64_t t = 1; t < T; ++t) th.emplace_back(guarded, t);
+  guarded(0);
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
 // gen.hpp:115-126 in parallel.  Pair (i, j) -- hot link i (ascending, as
 // sample_without_replacement sorts), stream j -- is decided by raw draw
 // P0 + i*n + j of the one sequential stream, so T threads each draw a
@@ -232,12 +254,7 @@ void hot_phase(std::uint64_t seed, std::uint64_t p0, const std::vector<std::int3
     }
     h.j.resize(cnt);
   };
-  {
-    std::vector<std::thread> th;
-    for (std::int64_t t = 1; t < T; ++t) th.emplace_back(draw_range, t);
-    draw_range(0);
-    for (auto& x : th) x.join();
-  }
+  run_threads(T, draw_range);
   for (int v : ok)
     if (!v) throw std::runtime_error("gen_congested: mt19937_64 jump-ahead unavailable");
   mark("draws");
@@ -307,12 +324,7 @@ void hot_phase(std::uint64_t seed, std::uint64_t p0, const std::vector<std::int3
     }
     o.resize(pos);
   };
-  {
-    std::vector<std::thread> th;
-    for (std::int64_t t = 1; t < T; ++t) th.emplace_back(build, t);
-    build(0);
-    for (auto& x : th) x.join();
-  }
+  run_threads(T, build);
   mark("per-stream union");
   hits.clear();
   hits.shrink_to_fit();
@@ -330,17 +342,11 @@ void hot_phase(std::uint64_t seed, std::uint64_t p0, const std::vector<std::int3
     start[static_cast<std::size_t>(t) + 1] = acc;
   }
   inst->routes.resize(static_cast<std::size_t>(start[static_cast<std::size_t>(T)]));
-  {
-    std::vector<std::thread> th;
-    auto cp = [&](std::int64_t t) {
-      auto& o = out[static_cast<std::size_t>(t)];
-      std::copy(o.begin(), o.end(), inst->routes.begin() + start[static_cast<std::size_t>(t)]);
-      std::vector<std::int32_t>().swap(o);
-    };
-    for (std::int64_t t = 1; t < T; ++t) th.emplace_back(cp, t);
-    cp(0);
-    for (auto& x : th) x.join();
-  }
+  run_threads(T, [&](std::int64_t t) {
+    auto& o = out[static_cast<std::size_t>(t)];
+    std::copy(o.begin(), o.end(), inst->routes.begin() + start[static_cast<std::size_t>(t)]);
+    std::vector<std::int32_t>().swap(o);
+  });
   mark("concatenate");
 }
 

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <initializer_list>
 #include <string>
 #include <thread>
@@ -72,10 +73,21 @@ void parallel_for(int64_t count, F f) {
     f(0, count);
     return;
   }
+  // an exception inside a std::thread would terminate the process: each
+  // worker keeps its own, the first is rethrown after the join
+  std::vector<std::exception_ptr> err(static_cast<size_t>(nt));
   std::vector<std::thread> ts;
   for (int64_t t = 0; t < nt; ++t)
-    ts.emplace_back([&, t] { f(count * t / nt, count * (t + 1) / nt); });
+    ts.emplace_back([&, t] {
+      try {
+        f(count * t / nt, count * (t + 1) / nt);
+      } catch (...) {
+        err[static_cast<size_t>(t)] = std::current_exception();
+      }
+    });
   for (auto& th : ts) th.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
 }
 
 // io.hpp:179-208.  Pass 1 (sequential, header fields only) finds every
