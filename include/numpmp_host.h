@@ -78,6 +78,21 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
  * numpmp_gen_transit. */
 int numpmp_transit_meta(const numpmp_instance* inst, int64_t* n_ods, int32_t* od, int32_t* route,
                         int32_t* t0, int32_t* od_origin, int32_t* od_dest);
+/* The rest of TransitMetadata: the spatial edges (from, to) and each OD's
+ * routes as edge sequences (OD q: routes [od_route_ptr[q], od_route_ptr[q+1]),
+ * route r: route_edges[route_ptr[r] .. route_ptr[r+1])).  Size with the
+ * counts first; any pointer may be null.  Returns 0 or 2. */
+int numpmp_transit_graph(const numpmp_instance* inst, int64_t* n_edges, int64_t* n_routes, int64_t* n_route_edges,
+                         int32_t* edge_from, int32_t* edge_to, int64_t* od_route_ptr, int64_t* route_ptr,
+                         int32_t* route_edges);
+/* write_transit_metadata (io.hpp:444-467): the "NUMT 1" sidecar, the same
+ * bytes as the reference.  Returns 0 or 6 (IoError). */
+int numpmp_write_transit_metadata(const char* path, int32_t stations, int32_t time_bins, double bin_minutes,
+                                  double seats, int64_t dropped, int64_t n_edges, const int32_t* edge_from,
+                                  const int32_t* edge_to, int64_t n_ods, const int32_t* od_origin,
+                                  const int32_t* od_dest, const int64_t* od_route_ptr, const int64_t* route_ptr,
+                                  const int32_t* route_edges, int64_t n_streams, const int32_t* s_od,
+                                  const int32_t* s_route, const int32_t* s_t0);
 
 /* In-place capacity degradation with the reference's draw order. */
 int numpmp_degrade(int64_t m, double* capacities, double p_degrade, double factor, uint64_t seed);

@@ -245,6 +245,8 @@ class Reference:
         L.ref_degrade.argtypes = [P, D, D, C.c_uint64, C.POINTER(P)]
         L.ref_transit_meta.argtypes = [P, C.POINTER(I64), P, P, P, P, P]
         L.ref_write_trace_csv.argtypes = [C.c_char_p, I64, P, P, P, P, P]
+        L.ref_write_transit_metadata.argtypes = [P, C.c_char_p]
+        L.ref_check_transit_metadata.argtypes = [C.c_char_p]
         L.ref_transit_report.argtypes = [P, P, P, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(I64), P, P, P, P,
                                          I64]
         L.ref_fail_and_prune.argtypes = [P, D, C.c_uint64, C.POINTER(P)]
@@ -362,6 +364,9 @@ class RefProblem:
         origin, dest = np.empty(k.value, np.int32), np.empty(k.value, np.int32)
         self.ref.L.ref_transit_meta(self.h, C.byref(k), _p(od), _p(route), _p(t0), _p(origin), _p(dest))
         return od, route, t0, origin, dest
+
+    def write_transit_metadata(self, path):
+        self.ref._err(self.ref.L.ref_write_transit_metadata(self.h, os.fsencode(path)))
 
     def transit_report(self, x, lam, od, t0, csv_path):
         """transit_report rows (stream ids, pi, lambda_hat per row) and the

@@ -548,4 +548,22 @@ int ref_transit_report(void* h, const double* x, const double* lam, std::int32_t
   }
 }
 
+// io.hpp:444-540
+int ref_write_transit_metadata(void* h, const char* path) {
+  try {
+    write_transit_metadata(static_cast<RefProblem*>(h)->meta, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int ref_check_transit_metadata(const char* path) {  // read_transit_metadata; 0 or the IoError
+  try {
+    (void)read_transit_metadata(path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

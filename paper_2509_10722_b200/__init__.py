@@ -47,7 +47,9 @@ from .solver import (
 from .transit import (
     TransitReportRow,
     normalized_route_prices,
+    read_transit_metadata,
     transit_report,
+    write_transit_metadata,
     write_trace_csv,
     write_transit_report_csv,
 )
@@ -59,4 +61,5 @@ __all__ = [
     "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
     "check_termination", "objective", "recover_duals", "to_string", "update_rho",
     "TransitReportRow", "normalized_route_prices", "transit_report", "write_trace_csv", "write_transit_report_csv",
+    "read_transit_metadata", "write_transit_metadata",
 ]

@@ -144,6 +144,9 @@ SIGNATURES = {
     "numpmp_fail_and_prune": (C.c_int, [I64, I64, P, P, P, P, P, D, C.c_uint64, C.POINTER(P), P, P]),
     "numpmp_read_problem": (C.c_int, [C.c_char_p, C.POINTER(P)]),
     "numpmp_transit_meta": (C.c_int, [P, PI64, P, P, P, P, P]),
+    "numpmp_transit_graph": (C.c_int, [P, PI64, PI64, PI64, P, P, P, P, P]),
+    "numpmp_write_transit_metadata": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, D, D, I64, I64, P, P, I64, P, P,
+                                                P, P, P, I64, P, P, P]),
     "numpmp_write_trace_csv": (C.c_int, [C.c_char_p, I64, P, P, P, P, P]),
     "numpmp_write_problem": (C.c_int, [I64, I64, P, P, P, P, P, C.c_char_p, C.c_int]),
     "numpmp_validate": (I64, [I64, I64, P, P, P, P, P, C.c_char_p, I64]),

@@ -607,6 +607,19 @@ int numpmp_gen_transit(const numpmp_transit_spec* spec, numpmp_instance** out, i
     inst->capacities.assign(static_cast<std::size_t>(inst->m), spec->seats);
     inst->od_origin = std::move(od_o);
     inst->od_dest = std::move(od_d);
+    for (const auto& e : edges) {
+      inst->edge_from.push_back(e.first);
+      inst->edge_to.push_back(e.second);
+    }
+    inst->od_route_ptr.push_back(0);
+    inst->route_ptr.push_back(0);
+    for (const auto& routes : od_routes) {
+      for (const auto& route : routes) {
+        inst->route_edges.insert(inst->route_edges.end(), route.begin(), route.end());
+        inst->route_ptr.push_back(static_cast<std::int64_t>(inst->route_edges.size()));
+      }
+      inst->od_route_ptr.push_back(static_cast<std::int64_t>(inst->route_ptr.size()) - 1);
+    }
     inst->transit = true;
     if (dropped) *dropped = drop;
     *out = inst;
@@ -649,6 +662,27 @@ int numpmp_transit_meta(const numpmp_instance* inst, int64_t* n_ods, int32_t* od
   put(inst->t_t0, t0);
   put(inst->od_origin, od_origin);
   put(inst->od_dest, od_dest);
+  return 0;
+}
+
+int numpmp_transit_graph(const numpmp_instance* inst, int64_t* n_edges, int64_t* n_routes, int64_t* n_route_edges,
+                         int32_t* edge_from, int32_t* edge_to, int64_t* od_route_ptr, int64_t* route_ptr,
+                         int32_t* route_edges) {
+  if (!inst->transit) {
+    g_host_err = "transit metadata: not a transit instance";
+    return 2;
+  }
+  if (n_edges) *n_edges = static_cast<int64_t>(inst->edge_from.size());
+  if (n_routes) *n_routes = static_cast<int64_t>(inst->route_ptr.size()) - 1;
+  if (n_route_edges) *n_route_edges = static_cast<int64_t>(inst->route_edges.size());
+  auto put = [](const auto& v, auto* dst) {
+    if (dst) std::copy(v.begin(), v.end(), dst);
+  };
+  put(inst->edge_from, edge_from);
+  put(inst->edge_to, edge_to);
+  put(inst->od_route_ptr, od_route_ptr);
+  put(inst->route_ptr, route_ptr);
+  put(inst->route_edges, route_edges);
   return 0;
 }
 

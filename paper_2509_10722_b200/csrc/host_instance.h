@@ -16,6 +16,11 @@ struct numpmp_instance {
   // transit instances only (TransitMetadata, transit.hpp:41-57): per stream
   // the OD index, route index and departure bin; per usable OD its stations
   std::vector<std::int32_t> t_od, t_route, t_t0, od_origin, od_dest;
+  // the spatial edges (from, to) and each OD's routes as edge sequences:
+  // OD q's routes are [od_route_ptr[q], od_route_ptr[q+1]), route r's edges
+  // route_edges[route_ptr[r] .. route_ptr[r+1])
+  std::vector<std::int32_t> edge_from, edge_to, route_edges;
+  std::vector<std::int64_t> od_route_ptr, route_ptr;
   bool transit = false;
 };
 

@@ -381,4 +381,53 @@ int numpmp_write_trace_csv(const char* path, int64_t rows, const int64_t* iter, 
   return 0;
 }
 
+int numpmp_write_transit_metadata(const char* path, int32_t stations, int32_t time_bins, double bin_minutes,
+                                  double seats, int64_t dropped, int64_t n_edges, const int32_t* edge_from,
+                                  const int32_t* edge_to, int64_t n_ods, const int32_t* od_origin,
+                                  const int32_t* od_dest, const int64_t* od_route_ptr, const int64_t* route_ptr,
+                                  const int32_t* route_edges, int64_t n_streams, const int32_t* s_od,
+                                  const int32_t* s_route, const int32_t* s_t0) {
+  // io.hpp:444-467 ("NUMT 1" sidecar)
+  const std::string p(path);
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_host_err = "cannot write '" + p + "'";
+    return 6;
+  }
+  std::string buf = "NUMT 1 " + std::to_string(stations) + ' ' + std::to_string(time_bins) + ' ' +
+                    std::to_string(n_edges) + ' ' + std::to_string(n_ods) + ' ' + std::to_string(n_streams) + '\n';
+  buf += fmt_double(bin_minutes) + ' ' + fmt_double(seats) + ' ' + std::to_string(dropped) + '\n';
+  bool ok = true;
+  auto flush = [&](bool force) {
+    if (buf.size() >= (1u << 22) || force) {
+      ok = ok && std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+      buf.clear();
+    }
+  };
+  for (int64_t e = 0; e < n_edges; ++e) {
+    buf += std::to_string(edge_from[e]) + ' ' + std::to_string(edge_to[e]) + '\n';
+    flush(false);
+  }
+  for (int64_t q = 0; q < n_ods; ++q) {
+    const int64_t r0 = od_route_ptr[q], r1 = od_route_ptr[q + 1];
+    buf += std::to_string(od_origin[q]) + ' ' + std::to_string(od_dest[q]) + ' ' + std::to_string(r1 - r0) + '\n';
+    for (int64_t r = r0; r < r1; ++r) {
+      buf += std::to_string(route_ptr[r + 1] - route_ptr[r]);
+      for (int64_t i = route_ptr[r]; i < route_ptr[r + 1]; ++i) buf += ' ' + std::to_string(route_edges[i]);
+      buf += '\n';
+    }
+    flush(false);
+  }
+  for (int64_t j = 0; j < n_streams; ++j) {
+    buf += std::to_string(s_od[j]) + ' ' + std::to_string(s_route[j]) + ' ' + std::to_string(s_t0[j]) + '\n';
+    flush(false);
+  }
+  flush(true);
+  if (std::fclose(f) != 0 || !ok) {
+    g_host_err = "write failed on '" + p + "'";
+    return 6;
+  }
+  return 0;
+}
+
 }  // extern "C"

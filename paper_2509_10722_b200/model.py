@@ -248,6 +248,13 @@ class TransitMetadata:  # transit.hpp:41-57 (edges and warnings not carried)
     stream_route: np.ndarray
     stream_t0: np.ndarray
     dropped_streams: int = 0
+    # spatial graph and OD routes (edge sequences): OD q's routes are
+    # [od_route_ptr[q], od_route_ptr[q+1]), route r's edges
+    # route_edges[route_ptr[r]:route_ptr[r+1]]
+    edges: Optional[np.ndarray] = None  # (E, 2) int32 (from, to)
+    od_route_ptr: Optional[np.ndarray] = None
+    route_ptr: Optional[np.ndarray] = None
+    route_edges: Optional[np.ndarray] = None
 
     def link_id(self, edge: int, t: int) -> int:
         return edge * self.time_bins + t
@@ -263,8 +270,15 @@ def _transit_meta(inst, spec: "TransitSpec", n: int, dropped: int) -> TransitMet
     origin, dest = np.empty(k.value, np.int32), np.empty(k.value, np.int32)
     L.numpmp_transit_meta(inst, C.byref(k), _lib.ptr(od), _lib.ptr(route), _lib.ptr(t0), _lib.ptr(origin),
                           _lib.ptr(dest))
+    ne, nr, nre = C.c_int64(), C.c_int64(), C.c_int64()
+    L.numpmp_transit_graph(inst, C.byref(ne), C.byref(nr), C.byref(nre), None, None, None, None, None)
+    ef, et = np.empty(ne.value, np.int32), np.empty(ne.value, np.int32)
+    orp, rp = np.empty(k.value + 1, np.int64), np.empty(nr.value + 1, np.int64)
+    re_ = np.empty(max(nre.value, 1), np.int32)[: nre.value]
+    L.numpmp_transit_graph(inst, C.byref(ne), C.byref(nr), C.byref(nre), _lib.ptr(ef), _lib.ptr(et), _lib.ptr(orp),
+                           _lib.ptr(rp), _lib.ptr(re_))
     return TransitMetadata(spec.stations, spec.time_bins, spec.bin_minutes, spec.seats, origin, dest, od, route, t0,
-                           dropped)
+                           dropped, np.stack([ef, et], axis=1), orp, rp, re_)
 
 
 def gen_transit(spec: TransitSpec, with_meta: bool = False):

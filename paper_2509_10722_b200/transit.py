@@ -9,6 +9,7 @@ the reference.
 from __future__ import annotations
 
 import os
+import re
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -98,3 +99,103 @@ def write_trace_csv(trace, path: str) -> None:
     rc = L.numpmp_write_trace_csv(os.fsencode(path), n, _lib.ptr(it), *[_lib.ptr(c) for c in cols])
     if rc:
         raise IoError(L.numpmp_host_last_error().decode())
+
+
+def write_transit_metadata(meta: TransitMetadata, path: str) -> None:
+    """io.hpp:444-467: the "NUMT 1" sidecar, the same bytes as the reference."""
+    if meta.edges is None:
+        raise ValidationError("transit metadata: no spatial graph (use gen_transit(..., with_meta=True))")
+    e = np.ascontiguousarray(meta.edges, np.int32)
+    ef, et = np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1])
+    arrs = dict(origin=np.ascontiguousarray(meta.od_origin, np.int32), dest=np.ascontiguousarray(meta.od_dest, np.int32),
+                orp=np.ascontiguousarray(meta.od_route_ptr, np.int64), rp=np.ascontiguousarray(meta.route_ptr, np.int64),
+                re=np.ascontiguousarray(meta.route_edges, np.int32), od=np.ascontiguousarray(meta.stream_od, np.int32),
+                route=np.ascontiguousarray(meta.stream_route, np.int32), t0=np.ascontiguousarray(meta.stream_t0, np.int32))
+    L = _lib.lib()
+    rc = L.numpmp_write_transit_metadata(
+        os.fsencode(path), meta.stations, meta.time_bins, meta.bin_minutes, meta.seats, meta.dropped_streams,
+        len(ef), _lib.ptr(ef), _lib.ptr(et), len(arrs["origin"]), _lib.ptr(arrs["origin"]), _lib.ptr(arrs["dest"]),
+        _lib.ptr(arrs["orp"]), _lib.ptr(arrs["rp"]), _lib.ptr(arrs["re"]), len(arrs["od"]), _lib.ptr(arrs["od"]),
+        _lib.ptr(arrs["route"]), _lib.ptr(arrs["t0"]))
+    if rc:
+        raise IoError(L.numpmp_host_last_error().decode())
+
+
+_INT = re.compile(r"^[+-]?[0-9]+$")
+
+
+def read_transit_metadata(path: str) -> TransitMetadata:
+    """io.hpp:469-540 with the reference's IoError messages."""
+    try:
+        f = open(path, "r", newline="\n")
+    except OSError:
+        raise IoError(f"cannot open '{path}'") from None
+    with f:
+        lines = f.read().split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    pos = [0]
+
+    def toks():
+        if pos[0] >= len(lines):
+            raise IoError(f"parse error at line {pos[0] + 1}: unexpected end of '{path}'")
+        pos[0] += 1
+        return lines[pos[0] - 1].split()
+
+    def pint(t, line):
+        if not _INT.match(t):
+            raise IoError(f"parse error at line {line}: expected an integer, got '{t}'")
+        return int(t)
+
+    def pdbl(t, line):
+        try:
+            if "_" in t:
+                raise ValueError
+            return float(t)
+        except ValueError:
+            raise IoError(f"parse error at line {line}: expected a number, got '{t}'") from None
+
+    head = toks()
+    if len(head) != 7 or head[0] != "NUMT":
+        raise IoError("parse error at line 1: expected 'NUMT 1 <S> <T> <E> <ods> <streams>'")
+    if pint(head[1], 1) != 1:
+        raise IoError("parse error at line 1: unsupported metadata version")
+    S, T, ne, nods, ns = (pint(h, 1) for h in head[2:7])
+    extra = toks()
+    if len(extra) != 3:
+        raise IoError("parse error at line 2: expected '<bin_minutes> <seats> <dropped>'")
+    bin_minutes, seats, dropped = pdbl(extra[0], 2), pdbl(extra[1], 2), pint(extra[2], 2)
+    edges = np.empty((ne, 2), np.int32)
+    for e in range(ne):
+        t = toks()
+        if len(t) != 2:
+            raise IoError(f"parse error at line {pos[0]}: expected '<from> <to>'")
+        edges[e] = (pint(t[0], pos[0]), pint(t[1], pos[0]))
+    origin, dest = np.empty(nods, np.int32), np.empty(nods, np.int32)
+    orp, rp, redges = [0], [0], []
+    for q in range(nods):
+        t = toks()
+        if len(t) != 3:
+            raise IoError(f"parse error at line {pos[0]}: expected '<origin> <dest> <routes>'")
+        origin[q], dest[q] = pint(t[0], pos[0]), pint(t[1], pos[0])
+        nr = pint(t[2], pos[0])
+        for _ in range(nr):
+            rt = toks()
+            line = pos[0]
+            if not rt:
+                raise IoError(f"parse error at line {line}: expected a route")
+            n = pint(rt[0], line)
+            if len(rt) != 1 + n:
+                raise IoError(f"parse error at line {line}: route length mismatch")
+            redges.extend(pint(x, line) for x in rt[1:])
+            rp.append(len(redges))
+        orp.append(len(rp) - 1)
+    trip = np.empty((ns, 3), np.int32)
+    for j in range(ns):
+        t = toks()
+        if len(t) != 3:
+            raise IoError(f"parse error at line {pos[0]}: expected '<od> <route> <t0>'")
+        trip[j] = (pint(t[0], pos[0]), pint(t[1], pos[0]), pint(t[2], pos[0]))
+    return TransitMetadata(S, T, bin_minutes, seats, origin, dest, np.ascontiguousarray(trip[:, 0]),
+                           np.ascontiguousarray(trip[:, 1]), np.ascontiguousarray(trip[:, 2]), dropped, edges,
+                           np.asarray(orp, np.int64), np.asarray(rp, np.int64), np.asarray(redges, np.int32))

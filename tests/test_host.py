@@ -399,3 +399,57 @@ def test_trace_csv_bytes_match_reference(reference, tmp_path):
     assert open(mine, "rb").read() == b"iter,r_norm,s_norm,rho,objective\n"
     with pytest.raises(pmp.IoError, match=r"^cannot write '/nonexistent/dir/t\.csv'$"):
         pmp.write_trace_csv(trace, "/nonexistent/dir/t.csv")
+
+
+@pytest.mark.parametrize("args", TRANSIT_REPORT_CASES)
+def test_transit_metadata_file_matches_reference(args, reference, tmp_path):
+    # io.hpp:444-540: the NUMT sidecar, byte-identical, and read back
+    p, meta = pmp.gen_transit(pmp.TransitSpec(*args), with_meta=True)
+    mine, theirs = str(tmp_path / "mine.numt"), str(tmp_path / "ref.numt")
+    pmp.write_transit_metadata(meta, mine)
+    reference.gen_transit(*args).write_transit_metadata(theirs)
+    assert open(mine, "rb").read() == open(theirs, "rb").read()
+    back = pmp.read_transit_metadata(mine)
+    for f in ("stream_od", "stream_route", "stream_t0", "od_origin", "od_dest", "edges", "od_route_ptr", "route_ptr",
+              "route_edges"):
+        np.testing.assert_array_equal(getattr(back, f), getattr(meta, f))
+    assert (back.stations, back.time_bins, back.bin_minutes, back.seats, back.dropped_streams) == \
+        (meta.stations, meta.time_bins, meta.bin_minutes, meta.seats, meta.dropped_streams)
+    # the report from the read-back metadata is the same
+    x, lam = np.linspace(0.5, 2.0, p.n), np.linspace(0.0, 1.0, p.m)
+    t0 = int(meta.stream_t0[0])
+    assert pmp.transit_report(p, x, lam, back, 0, t0) == pmp.transit_report(p, x, lam, meta, 0, t0)
+
+
+def test_transit_metadata_reader_errors_match_reference(reference, tmp_path):
+    from oracle.oracle import Reference  # noqa: F401 (reference fixture already built)
+
+    good = str(tmp_path / "good.numt")
+    p, meta = pmp.gen_transit(pmp.TransitSpec(*TRANSIT_REPORT_CASES[0]), with_meta=True)
+    pmp.write_transit_metadata(meta, good)
+    lines = open(good).read().split("\n")
+    n_edges = int(lines[0].split()[4])
+    cases = {
+        "magic": ["NUMX" + lines[0][4:]] + lines[1:],
+        "version": [lines[0].replace("NUMT 1", "NUMT 2", 1)] + lines[1:],
+        "head_int": [lines[0].replace("NUMT 1 ", "NUMT 1 x", 1)] + lines[1:],
+        "extra": [lines[0], "5 50"] + lines[2:],
+        "extra_num": [lines[0], "5 fifty 0"] + lines[2:],
+        "edge": lines[:2] + ["1 2 3"] + lines[3:],
+        "od": lines[:2 + n_edges] + ["1 2"] + lines[3 + n_edges:],
+        "route_len": lines[:3 + n_edges] + ["9 1 2"] + lines[4 + n_edges:],
+        "stream": lines[:-3] + ["1 2"] + lines[-2:],
+        "truncated": lines[: len(lines) // 2],
+    }
+    for name, ls in cases.items():
+        path = str(tmp_path / f"{name}.numt")
+        with open(path, "w") as f:
+            f.write("\n".join(ls))
+        rc = reference.L.ref_check_transit_metadata(os.fsencode(path))
+        assert rc != 0, name
+        want = reference.L.ref_last_error().decode()
+        with pytest.raises(pmp.IoError) as e:
+            pmp.read_transit_metadata(path)
+        assert str(e.value) == want, name
+    with pytest.raises(pmp.IoError, match=r"^cannot open '/nonexistent/m\.numt'$"):
+        pmp.read_transit_metadata("/nonexistent/m.numt")
