@@ -852,8 +852,11 @@ __device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
 // epilogue.  Rows never cross units, so no second combine pass exists.
 // kForm: 0 row mode, 1 warp units, 2 warp units + split-row pieces (separate
 // instantiations: neither form's code shapes another's register allocation).
+#ifndef NUMPMP_ROW_MINB
+#define NUMPMP_ROW_MINB NUMPMP_MIN_BLOCKS
+#endif
 template <int kPhase, int kForm>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
+__global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
   __shared__ __align__(16) int sidx[kWarps][kStageInts];

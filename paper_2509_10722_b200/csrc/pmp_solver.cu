@@ -246,6 +246,7 @@ struct numpmp_gpu {
 
   int cur = 0;  // index of the current iterate buffers
   int grid1 = 0, grid2 = 0, grid3 = 0;
+  int grid2r = 0;  // link pass in row mode (its own occupancy)
   int64_t iters_since_upload = 0;
   bool host_p_valid = false;  // set_state keeps p / p_bar verbatim for get_state
   std::vector<double> host_p, host_pbar;
@@ -401,7 +402,7 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
 template <int kPhase>
 void launch_link_pass(const numpmp_gpu* h, const IterArgs& a, const BlockArgs& bk, const double* src, double* out) {
   if (bk.row_mode)
-    k_link_pass<kPhase, 0><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
+    k_link_pass<kPhase, 0><<<h->grid2r, kThreads, 0, h->stream>>>(a, bk, src, out);
   else if (bk.npieces == 0)
     k_link_pass<kPhase, 1><<<h->grid2, kThreads, 0, h->stream>>>(a, bk, src, out);
   else
@@ -934,8 +935,9 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 2>, kThreads, 0));
-  int occ3 = 0;
+  int occ3 = 0, occ2r = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2r, k_link_pass<LP_ACC, 0>, kThreads, 0));
   int64_t max_bs = 0, max_nu = 0;
   for (const ColBlock& cb : h->blocks) {
     max_bs = std::max(max_bs, cb.s1 - cb.s0);
@@ -951,10 +953,12 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
       1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, gmult * sms * std::max(occ2, 1))));
   h->grid3 = static_cast<int>(std::max(
       1LL, std::min<long long>((m + kThreads - 1) / kThreads, 1LL * sms * std::max(occ3, 1))));
+  h->grid2r = static_cast<int>(std::max(
+      1LL, std::min<long long>(((m + 31) / 32 + kWarps - 1) / kWarps, gmult * sms * std::max(occ2r, 1))));
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
                                   2 * static_cast<size_t>(std::max(h->grid3, h->grid1)),
                               b, h->stream);
-  h->k2_part = dalloc<double>(4 * static_cast<size_t>(std::max(h->grid2, h->grid3)), b, h->stream);
+  h->k2_part = dalloc<double>(4 * static_cast<size_t>(std::max({h->grid2, h->grid2r, h->grid3})), b, h->stream);
   h->trace_cap = h->cfg.max_iters / h->cfg.trace_every + 2;
   h->trace_dev = dalloc<numpmp_trace_row>(static_cast<size_t>(h->trace_cap), b, h->stream);
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&h->ev_batch[i], cudaEventDisableTiming));
