@@ -596,6 +596,53 @@ def test_config_c_full_solve_properties():
     assert np.min(sol.lambda_) >= 0.0
 
 
+def _config_f():
+    # bench config F: B size + 100 hot links on ~10% of the streams (split rows)
+    return pmp.gen_congested(pmp.GenSpec(m=100000, n=1000000, avg_links_per_stream=10.0, kind=pmp.GenKind.Mixed,
+                                         weights=pmp.WeightDist.uniform(0.5, 1.5), seed=7), 0.001, 0.10)
+
+
+@pytest.mark.slow
+def test_config_f_first_iterations_match_oracle(restatement, oracle_mod):
+    # the congested config at full size (2e7 nonzeros, hot rows of ~1e5 entries), K = 20 iterations
+    p = _config_f()
+    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0, max_iters=20, trace_every=1)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert sol.iterations == ref.iterations == 20
+    for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
+    for row, want in zip(sol.trace, ref.trace):
+        assert abs(row.r_norm - want[1]) <= RTOL * want[1] and abs(row.s_norm - want[2]) <= RTOL * want[2]
+
+
+@pytest.mark.slow
+def test_config_f_full_solve_properties():
+    # converged congested run: feasible within tolerance, x >= 0, prices >= 0,
+    # and bit-identical on a rerun (split-row pieces combine in a fixed order)
+    p = _config_f()
+    cfg = pmp.SolverConfig(eps_abs=1e-4, rho0=1000.0)
+    with pmp.PmpSolver(p, cfg) as s:
+        sol = s.solve()
+        again = s.solve()
+    assert sol.status == pmp.SolveStatus.Converged
+    np.testing.assert_array_equal(sol.x, again.x)
+    eps_tol = 1e-4 * math.sqrt(p.nnz + p.m)
+    assert sol.r_norm < eps_tol and sol.s_norm < eps_tol
+    load = np.bincount(p.route_links, weights=np.repeat(sol.x, np.diff(p.stream_offsets)), minlength=p.m)
+    viol = np.abs(load + sol.s - p.capacities)
+    # r^2 = sum_l (d_l + 1) pbar_l^2 bounds a link's load residual (d_l + 1) pbar_l by
+    # sqrt(d_l + 1) r: the violation a converged run may leave grows with the degree
+    deg = np.bincount(p.route_links, minlength=p.m)
+    normal = deg <= 2 * p.nnz / p.m
+    assert np.max(viol[normal]) <= 10.0 * eps_tol
+    assert np.all(viol <= np.sqrt(deg + 1.0) * eps_tol)
+    assert np.min(sol.x) >= -1e-4
+    assert np.min(sol.lambda_) >= 0.0
+
+
 def _ipc_rank(rank, world, port, q):
     # one process per rank, all on cuda:0 (the box has one GPU): the real
     # CUDA IPC path of the exchange (export -> all_gather -> open), gloo for
