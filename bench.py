@@ -34,25 +34,25 @@ UNIT = "iterations/s"
 
 # BASELINE.json configs / SURVEY.md Appendix B (reference generators, fixed seeds)
 CONFIGS = {
-    "A": dict(m=1000, n=10000, avg=5.0, kind=0, uniform=False, seed=7, rho0=1000.0,
+    "A": dict(ref_iters=50000, m=1000, n=10000, avg=5.0, kind=0, uniform=False, seed=7, rho0=1000.0,
               desc="A: 10k streams / 1k links, log, w=1"),
-    "B": dict(m=100000, n=1000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
+    "B": dict(ref_iters=100, m=100000, n=1000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
               desc="B: 1M streams / 100k links, log, w=1"),
-    "C": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0,
+    "C": dict(ref_iters=12, m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0,
               desc="C: 10M streams / 1M links, mixed log+linear (Bernoulli 0.5), w~U(0.5,1.5)"),
-    "D": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, degrade=(0.5, 0.5, 99),
+    "D": dict(ref_iters=12, m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, degrade=(0.5, 0.5, 99),
               desc="D: C with 50% of capacities x0.5 (degrade seed 99)"),
-    "E": dict(transit=(100, 192, 5.0, 952, 9900, 9, 192, 50.0, 4), rho0=1000.0,
+    "E": dict(ref_iters=20, transit=(100, 192, 5.0, 952, 9900, 9, 192, 50.0, 4), rho0=1000.0,
               desc="E: time-expanded transit, S=100 T=192 |E|=952, 9900 OD x 9 routes x 192 departures, seats 50"),
     # SURVEY.md 8(d) optional paper-shape cross-check (1847 s on an A100, tolerance and
     # iteration count unstated): more links than streams
     # gen_congested (hot links on 10% of the streams each): the heavy-tailed
     # streams-per-link distribution; hot rows are split over several warp units in the link pass
-    "F": dict(m=100000, n=1000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, congested=(0.001, 0.10),
+    "F": dict(ref_iters=50, m=100000, n=1000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, congested=(0.001, 0.10),
               desc="F: B-size congested, 100 hot links on ~10% of 1M streams each (mixed, w~U(0.5,1.5))"),
-    "G": dict(m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, congested=(0.001, 0.10),
+    "G": dict(ref_iters=2, m=1000000, n=10000000, avg=10.0, kind=2, uniform=True, seed=7, rho0=1000.0, congested=(0.001, 0.10),
               desc="G: C congested, 1000 hot links on ~10% of 10M streams each (1.1e9 nonzeros)"),
-    "P": dict(m=10000000, n=5000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
+    "P": dict(ref_iters=12, m=10000000, n=5000000, avg=10.0, kind=0, uniform=False, seed=7, rho0=1000.0,
               desc="P: paper shape, 5M streams / 10M links, log, w=1"),
 }
 
@@ -80,6 +80,30 @@ def make_problem(name):
     if "degrade" in c:
         p = pmp.degrade(p, *c["degrade"])
     return p
+
+
+DATA = "synthetic (the reference generator recipe of the config, fixed seed)"
+
+
+def repo_libs_loaded():
+    """Shared objects under this repo mapped into this process (/proc/self/maps)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                path = ln.split()[-1] if len(ln.split()) >= 6 else ""
+                if path.endswith(".so") and os.path.realpath(path).startswith(os.path.realpath(ROOT) + os.sep):
+                    out.add(os.path.relpath(os.path.realpath(path), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def bench_config(name, m, n, nnz):
+    """The `config` object both arms print (identical by construction)."""
+    return {"workload": CONFIGS[name]["desc"], "m": m, "n": n, "nnz": nnz, "eps_abs": 1e-4,
+            "rho0": CONFIGS[name]["rho0"], "alpha": 1.6, "mu": 2.0, "gamma": 1.1, "rho_update_interval": 50,
+            "l2": "inputs larger than L2 (>1 GB touched per iteration at C/D/E vs 126 MB L2)"}
 
 
 def solver_config(name, max_iters=50000):
@@ -212,40 +236,47 @@ def sum_over_ranks(world, value):
 
 
 # ------------------------------------------------------------- reference arm
-def reference_baseline(problem, name, iters, warmup=1):
-    """Time the reference CPU PmpSolver (oracle/_ref) on the same Problem.
-    Falls back to the plain-C restatement (1 core) if _ref is absent."""
+def make_ref_problem(name):
+    """The config's Problem built by the REFERENCE's own generators (oracle/_ref:
+    gen.hpp / transit.hpp compiled from /root/reference), so the reference arm
+    maps no library of this repo."""
+    from oracle import oracle as o
+
+    ref = o.Reference()
+    c = CONFIGS[name]
+    if "transit" in c:
+        return ref.gen_transit(*c["transit"])
+    w = ("uniform", 0.5, 1.5) if c["uniform"] else ("constant", 1.0, 1.0)
+    if "congested" in c:
+        rp = ref.gen(c["m"], c["n"], c["avg"], c["kind"], w, c["seed"], congested=True,
+                     hot_link_fraction=c["congested"][0], hot_stream_fraction=c["congested"][1])
+    else:
+        rp = ref.gen(c["m"], c["n"], c["avg"], c["kind"], w, c["seed"])
+    if "degrade" in c:
+        rp = rp.degrade(*c["degrade"])
+    return rp
+
+
+def reference_solves(rp, name, steps, warmup, iters):
+    """The reference's stock PmpSolver::solve() (solver.hpp:411, run 441-508 +
+    post-processing) on the held solver, cfg.max_iters = `iters` (a bounded
+    sample; small configs converge first), all host threads.  Returns
+    (seconds per step, iterations per step, cores)."""
     from oracle import oracle as o
 
     cores = os.cpu_count() or 1
-    cfg = o.Config(eps_abs=1e-4, rho0=CONFIGS[name]["rho0"], threads=cores)
-    if os.path.exists(o.REF_SO):
-        ref = o.Reference()
-        rp = ref.build_problem(problem.m, problem.n, problem.stream_offsets, problem.route_links, problem.kinds,
-                               problem.weights, problem.capacities)
-        sess = rp.bench_session(cfg)
-        if warmup:
-            sess.iterations(warmup)
-        secs = []
-        for _ in range(iters):
-            s, _ = sess.iterations(1)
-            secs.append(s)
-        sess.close()
-        kind = "reference"
-    else:
-        R = o.Restatement()
-        a = o.arrays_from(problem)
-        oc = o.Config(eps_abs=1e-4, rho0=CONFIGS[name]["rho0"])
-        st = R.cold_state(a, oc)
-        for _ in range(warmup):
-            R.step(a, oc, st)
-        secs = []
-        for _ in range(iters):
-            t = time.perf_counter()
-            R.step(a, oc, st)
-            secs.append(time.perf_counter() - t)
-        cores, kind = 1, "port"
-    return secs, cores, kind
+    cfg = o.Config(eps_abs=1e-4, rho0=CONFIGS[name]["rho0"], alpha=1.6, mu=2.0, gamma=1.1,
+                   rho_update_interval=50, max_iters=iters, trace_every=10, threads=cores)
+    sess = rp.bench_session(cfg)
+    for _ in range(warmup):
+        sess.solve()
+    secs, its = [], []
+    for _ in range(steps):
+        t, _, k = sess.solve()
+        secs.append(t)
+        its.append(k)
+    sess.close()
+    return secs, its, cores
 
 
 def run_reference_arm(args):
@@ -253,33 +284,70 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     name = args.config
-    problem = make_problem(name)
-    secs, cores, kind = reference_baseline(problem, name, args.steps, warmup=args.warmup)
+    from oracle import oracle as o
+
+    if not os.path.exists(o.REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnumpmp_ref.so not built"}), flush=True)
+        return 0
+    rp = make_ref_problem(name)
+    k = args.ref_iters or CONFIGS[name]["ref_iters"]
+    secs, its, cores = reference_solves(rp, name, args.steps, args.warmup, k)
     total = float(sum(secs))
-    value = args.steps / total if total > 0 else None
-    sample = (f"{args.steps} timed iterations (+{args.warmup} warm-up) of the reference PmpSolver run loop "
-              f"(solver.hpp:450-476) from the cold state on config {name}; {cores} host threads")
+    value = sum(its) / total if total > 0 else None
+    sample = (f"each step = the reference's stock PmpSolver::solve() (solver.hpp:411,441-508) from the cold state "
+              f"with max_iters={k} on config {name} (eps_abs 1e-4; iterations per step {its}), problem from the "
+              f"reference's own generator, {cores} host threads; steady_clock around solve() only")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator recipe, fixed seed)",
-        "config": {"workload": CONFIGS[name]["desc"], "m": problem.m, "n": problem.n, "nnz": problem.nnz,
-                   "eps_abs": 1e-4, "rho0": CONFIGS[name]["rho0"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "data": DATA,
+        "config": bench_config(name, rp.m, rp.n, rp.nnz),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iterations_per_step": its,
+        "repo_libs_loaded": repo_libs_loaded(),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------ our arm
+def rank_topology(solver, rank, world, local, exchange):
+    """Proof that all N ranks connected: per rank its device, PCI bus id,
+    peer access to every other rank's device, its stream range and (p2p) the
+    links it owns.  Gathered on every rank (collective)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2509_10722_b200.shard import link_owners
+
+    devs = [None] * world
+    dist.all_gather_object(devs, local)
+    mine = {"rank": rank, "device": local, "pci_bus_id": getattr(torch.cuda.get_device_properties(local), "pci_bus_id", None),
+            "streams": [solver.stream_begin, solver.stream_begin + solver.local.n],
+            "peer_access": [True if d == local else bool(torch.cuda.can_device_access_peer(local, d)) for d in devs]}
+    if exchange == "p2p":
+        b = link_owners(solver.full.m, world)
+        mine["links_owned"] = [int(b[rank]), int(b[rank + 1])]
+    out = [None] * world
+    dist.all_gather_object(out, mine)
+    return {"world": world, "exchange": exchange, "distinct_devices": len(set(devs)), "ranks": out}
+
+
 def run_ours(args):
     import paper_2509_10722_b200 as pmp
     from paper_2509_10722_b200 import _lib
     from paper_2509_10722_b200.shard import ShardedPmpSolver, nccl_unique_id
 
     rank, world, local = dist_setup(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
+    same_device = os.environ.get("NUMPMP_BENCH_SAME_DEVICE") == "1"
+    if world > 1 and not same_device:
+        import torch
+
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} GPUs visible")
     name = args.config
     t_gen = time.perf_counter()
     problem = make_problem(name)
@@ -304,9 +372,11 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         return ShardedPmpSolver(problem, cfg, rank, world, obj[0], device=local, exchange="nccl")
 
+    topology = None
     if world > 1:
         solver = make_sharded()
         h = solver.handle()
+        topology = rank_topology(solver, rank, world, local, exchange)
     else:
         solver = pmp.PmpSolver(problem, cfg, device=local)
         h = solver.handle()
@@ -455,24 +525,31 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        secs, cores, kind = reference_baseline(problem, name, args.cpu_iters, warmup=1)
-        cpu = {"value": len(secs) / sum(secs), "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"{len(secs)} iterations (+1 warm-up) of the reference run loop on config {name}, "
-                         f"{cores} host threads ({'oracle/_ref = reference headers compiled -O3' if kind == 'reference' else 'oracle restatement, 1 core'})"}
+        from oracle import oracle as o
+
+        if os.path.exists(o.REF_SO):
+            rp = o.Reference().build_problem(problem.m, problem.n, problem.stream_offsets, problem.route_links,
+                                             problem.kinds, problem.weights, problem.capacities)
+            k = args.ref_iters or CONFIGS[name]["ref_iters"]
+            secs, its, cores = reference_solves(rp, name, 1, 0, k)
+            del rp
+            cpu = {"value": sum(its) / sum(secs), "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"one stock PmpSolver::solve() of the reference (oracle/_ref = reference headers "
+                             f"compiled -O3) with max_iters={k} ({its[0]} iterations) on config {name}, "
+                             f"{cores} host threads"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": (topology["distinct_devices"] if topology else 1), "ranks": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generator recipe gen_uncongested, fixed seed; regenerated bit-exactly)",
-            "config": {"workload": CONFIGS[name]["desc"], "m": problem.m, "n": problem.n, "nnz": problem.nnz,
-                       "eps_abs": 1e-4, "rho0": CONFIGS[name]["rho0"], "alpha": 1.6,
-                       "parallelism": f"stream shards x{world}" + (
-                           (" + fused peer-memory exchange (NVLink stores into link owners, owner epilogue)"
-                            if exchange == "p2p" else " + NCCL all-reduce of link loads") if world > 1 else ""),
-                       "l2": "inputs larger than L2 (>1.3 GB touched per iteration vs 126 MB L2)",
-                       "step": "one cold-start solve to eps_abs=1e-4 (time-to-tolerance)"},
+            "data": DATA,
+            "config": bench_config(name, problem.m, problem.n, problem.nnz),
+            "parallelism": f"stream shards x{world}" + (
+                (" + fused peer-memory exchange (NVLink stores into link owners, owner epilogue)"
+                 if exchange == "p2p" else " + NCCL all-reduce of link loads") if world > 1 else ""),
+            "step": "one cold-start solve to eps_abs=1e-4 (time-to-tolerance)",
             "iterations_per_solve": iters, "status": statuses,
             "time_to_tol_s": ms_per_step / 1e3,
             "ms_per_iteration": total_ms / max(total_iters, 1),
@@ -498,7 +575,11 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
+            "topology": topology,
+            "repo_libs_loaded": repo_libs_loaded(),
         }
+        if same_device and world > 1:
+            line["functional_only"] = True  # ranks time-share one GPU: not a scaling result
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -508,6 +589,19 @@ def run_ours(args):
     return 0
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1; rank 0's JSON line is passed through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -515,11 +609,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--ref-iters", type=int, default=0,
+                    help="max_iters of each reference solve (0: the config's default sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_ours(args)
 
 

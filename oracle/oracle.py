@@ -263,7 +263,7 @@ class Reference:
         L.ref_warm_after_degrade.argtypes = [P, P, P, P, D, P, P, P]
         L.ref_warm_after_prune.argtypes = [P, P, I64, P, I64, D, P, P, P]
         L.ref_bench_open.argtypes = [P, P, P, C.POINTER(P)]
-        L.ref_bench_iters.argtypes = [P, I64, P, P]
+        L.ref_bench_solve.argtypes = [P, P, P, P]
         L.ref_bench_close.argtypes = [P]
         L.ref_prox_log.restype = D
         L.ref_prox_log.argtypes = [D, D, D, I64]
@@ -478,7 +478,7 @@ class RefProblem:
 
 
 class RefBenchSession:
-    """A reference PmpSolver held open for timing (ref_bench_*)."""
+    """A reference PmpSolver held open for timing its stock solve() (ref_bench_*)."""
 
     def __init__(self, rp: RefProblem, cfg: Config):
         self.rp = rp
@@ -486,11 +486,13 @@ class RefBenchSession:
         self.h = P()
         rp.ref._err(rp.ref.L.ref_bench_open(rp.h, _p(d), _p(i), C.byref(self.h)))
 
-    def iterations(self, k: int):
+    def solve(self):
+        """One stock PmpSolver::solve() on the held solver: (seconds, status, iterations)."""
         secs = np.zeros(1)
-        last = np.zeros(2)
-        self.rp.ref._err(self.rp.ref.L.ref_bench_iters(self.h, k, _p(secs), _p(last)))
-        return float(secs[0]), last
+        ints = np.zeros(2, np.int64)
+        rs = np.zeros(2)
+        self.rp.ref._err(self.rp.ref.L.ref_bench_solve(self.h, _p(secs), _p(ints), _p(rs)))
+        return float(secs[0]), int(ints[0]), int(ints[1])
 
     def close(self):
         if self.h:

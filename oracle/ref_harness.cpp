@@ -419,18 +419,13 @@ int ref_warm_after_prune(void* pruned, const double* prior_x, std::int64_t prior
   }
 }
 
-// Persistent CPU-baseline session: one PmpSolver (constructed once, as a
-// user would) stepping the reference run loop body (solver.hpp:450-476)
-// from the cold state; ref_bench_iters times `k` more iterations.
+// Persistent CPU-baseline session: one PmpSolver constructed once (as a user
+// would), with cfg.max_iters = the sample size; every ref_bench_solve call is
+// the stock PmpSolver::solve() (solver.hpp:411 -> cold_state, run 441-508,
+// post-processing), timed with steady_clock around solve() only.
 struct RefBench {
-  const Problem* prob;
-  SolverConfig cfg;
   PmpSolver solver;
-  SolverState st;
-  std::int64_t iter = 0;
-  RefBench(const Problem& p, const SolverConfig& c) : prob(&p), cfg(c), solver(p, c) {
-    st = solver.cold_state();
-  }
+  RefBench(const Problem& p, const SolverConfig& c) : solver(p, c) {}
 };
 
 int ref_bench_open(void* h, const double* cfgd, const std::int64_t* cfgi, void** out) {
@@ -442,24 +437,18 @@ int ref_bench_open(void* h, const double* cfgd, const std::int64_t* cfgi, void**
   }
 }
 
-int ref_bench_iters(void* bh, std::int64_t k, double* seconds, double* last_rs) {
+// ints = {status, iterations}; rs = {r_norm, s_norm}
+int ref_bench_solve(void* bh, double* seconds, std::int64_t* ints, double* rs) {
   try {
     auto* b = static_cast<RefBench*>(bh);
-    std::vector<double> prev_z;
-    double r = 0.0, s = 0.0;
     const auto t0 = std::chrono::steady_clock::now();
-    for (std::int64_t i = 0; i < k; ++i) {
-      const std::int64_t it = ++b->iter;
-      prev_z = b->st.z;
-      auto rs = b->solver.step(b->st);
-      r = rs.first;
-      s = rs.second;
-      if (it % b->cfg.rho_update_interval == 0) update_rho(b->st, r, s, b->solver.config());
-    }
+    const Solution sol = b->solver.solve();
     *seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    last_rs[0] = r;
-    last_rs[1] = s;
+    ints[0] = static_cast<std::int64_t>(sol.status);
+    ints[1] = sol.iterations;
+    rs[0] = sol.r_norm;
+    rs[1] = sol.s_norm;
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

@@ -453,3 +453,27 @@ def test_transit_metadata_reader_errors_match_reference(reference, tmp_path):
         assert str(e.value) == want, name
     with pytest.raises(pmp.IoError, match=r"^cannot open '/nonexistent/m\.numt'$"):
         pmp.read_transit_metadata("/nonexistent/m.numt")
+
+
+def test_bench_reference_arm_is_the_reference_alone():
+    # bench.py --impl reference: the reference's own generator and stock
+    # PmpSolver::solve() (oracle/_ref); no library of this repo is mapped, and
+    # the config object is the one the GPU arm prints.
+    import json
+    import subprocess
+    import sys
+
+    import bench
+
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref_so = os.path.join(ROOT, "oracle", "_ref", "libnumpmp_ref.so")
+    if not os.path.exists(ref_so):
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "A",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, check=True)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["repo_libs_loaded"] == ["oracle/_ref/libnumpmp_ref.so"]
+    assert line["config"] == bench.bench_config("A", 1000, 10000, 49795)
+    assert line["iterations_per_step"] == [423]  # config A converges inside the sample
+    assert line["cpu_baseline"]["kind"] == "reference"
