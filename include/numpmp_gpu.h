@@ -171,7 +171,10 @@ int numpmp_gpu_path_prices(numpmp_gpu* h, const double* lambda, double* pi);
 /* Loads an arbitrary reference SolverState (solver.hpp:51-62): p, z of
  * length J = nnz + m, p_bar and price of length m.  z must decompose as
  * z_t = A_j - B_l over the incidence (every cold, warm and stepped state
- * does); otherwise NUMPMP_INVALID_ARGUMENT. */
+ * does); otherwise NUMPMP_INVALID_ARGUMENT.  The state the handle issued
+ * last through numpmp_gpu_get_state (all four arrays), with nothing run
+ * since, is recognised by a fingerprint and kept as is: no host
+ * decomposition, no upload, and the device state stays bit-identical. */
 int numpmp_gpu_set_state(numpmp_gpu* h, const double* p, const double* z, const double* p_bar,
                          const double* price, double rho, int64_t iter);
 
@@ -181,8 +184,20 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
                          double* rho, int64_t* iter, double* prev_z);
 
 /* Replaces PmpSolver::step (solver.hpp:316-409): one iteration with no
- * termination test, trace or rho balancing; returns (r_norm, s_norm). */
+ * termination test, trace or rho balancing; returns (r_norm, s_norm) of
+ * residuals(after, before) -- on single-device handles computed by exactly
+ * the reduction numpmp_gpu_residuals runs, so the two agree bit for bit on
+ * the states get_state returns (solver.hpp:316-318, test_solver.cpp:245-262).
+ * A run's `done` flag is cleared first (step after run iterates). */
 int numpmp_gpu_step(numpmp_gpu* h, double* r_norm, double* s_norm);
+
+/* Replaces the free function residuals(state, prev, layout)
+ * (solver.hpp:139-154): r = sqrt(sum_l |l| p_bar_l^2), s = sqrt(sum_t
+ * (rho (z_t - prev_z_t))^2) over the handle's layout, as a fixed-order device
+ * reduction.  p_bar[m], z[J], prev_z[J]; rho is the after-state's rho.
+ * Single-device handles only. */
+int numpmp_gpu_residuals(numpmp_gpu* h, const double* p_bar, const double* z, const double* prev_z,
+                         double rho, double* r_norm, double* s_norm);
 
 /* Replaces PmpSolver::run (solver.hpp:441-508) from the current state
  * (call set_cold / set_warm first; solve() == set_cold + run).  x[n],

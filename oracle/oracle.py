@@ -265,6 +265,7 @@ class Reference:
         L.ref_bench_open.argtypes = [P, P, P, C.POINTER(P)]
         L.ref_bench_solve.argtypes = [P, P, P, P]
         L.ref_bench_close.argtypes = [P]
+        L.ref_groups.argtypes = [P, C.POINTER(I64), C.POINTER(I64), P, P, P, P]
         L.ref_prox_log.restype = D
         L.ref_prox_log.argtypes = [D, D, D, I64]
         L.ref_prox_linear_nonneg.restype = D
@@ -351,6 +352,16 @@ class RefProblem:
         self.ref.L.ref_export(self.h, _p(a.capacities), _p(a.weights), _p(a.kinds), _p(a.stream_offsets),
                               _p(a.terminal_link), _p(a.link_offsets), _p(a.link_terminals), _p(a.link_counts))
         return a
+
+    def groups(self):
+        """group_streams (model.hpp:255-286): list of (tau, kind, members)."""
+        ng, nm = I64(), I64()
+        self.ref.L.ref_groups(self.h, C.byref(ng), C.byref(nm), None, None, None, None)
+        tau, kind = np.empty(ng.value, np.int32), np.empty(ng.value, np.int32)
+        cnt, mem = np.empty(ng.value, np.int64), np.empty(nm.value, np.int64)
+        self.ref.L.ref_groups(self.h, C.byref(ng), C.byref(nm), _p(tau), _p(kind), _p(cnt), _p(mem))
+        ends = np.cumsum(cnt)
+        return [(int(t), int(k), mem[e - c:e]) for t, k, c, e in zip(tau, kind, cnt, ends)]
 
     def write_problem(self, path, encoding="auto"):
         self.ref._err(self.ref.L.ref_write_problem(self.h, os.fsencode(path),

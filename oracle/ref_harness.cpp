@@ -455,6 +455,26 @@ int ref_bench_solve(void* bh, double* seconds, std::int64_t* ints, double* rs) {
   }
 }
 
+// group_streams (model.hpp:255-286) flattened: per group tau, kind, member
+// count; members concatenated in group order.  Call with null arrays first
+// for the sizes.
+void ref_groups(void* h, std::int64_t* ngroups, std::int64_t* nmembers, std::int32_t* tau,
+                std::int32_t* kind, std::int64_t* count, std::int64_t* members) {
+  const auto gs = group_streams(static_cast<RefProblem*>(h)->p);
+  *ngroups = static_cast<std::int64_t>(gs.size());
+  std::int64_t k = 0;
+  for (std::size_t g = 0; g < gs.size(); ++g) {
+    if (tau) tau[g] = gs[g].tau;
+    if (kind) kind[g] = static_cast<std::int32_t>(gs[g].kind);
+    if (count) count[g] = static_cast<std::int64_t>(gs[g].members.size());
+    for (std::int64_t j : gs[g].members) {
+      if (members) members[k] = j;
+      ++k;
+    }
+  }
+  *nmembers = k;
+}
+
 void ref_bench_close(void* bh) { delete static_cast<RefBench*>(bh); }
 
 // prox.hpp scalars, for the prox golden vectors.

@@ -17,6 +17,7 @@ from .model import (
     TerminalLayout,
     TransitMetadata,
     TransitSpec,
+    TypeGroup,
     WeightDist,
     build_problem,
     PruneMap,
@@ -25,6 +26,7 @@ from .model import (
     gen_congested,
     gen_transit,
     gen_uncongested,
+    group_streams,
     problem_from_arrays,
     read_problem,
     validate,
@@ -56,8 +58,8 @@ from .transit import (
 
 __all__ = [
     "DeviceError", "DomainError", "GenError", "IoError", "SolverError", "ValidationError",
-    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitMetadata", "TransitSpec", "WeightDist",
-    "build_problem", "degrade", "fail_and_prune", "PruneMap", "gen_congested", "gen_transit", "gen_uncongested", "problem_from_arrays", "read_problem", "validate", "write_problem",
+    "GenKind", "GenSpec", "Problem", "Stream", "StreamKind", "TerminalLayout", "TransitMetadata", "TransitSpec", "TypeGroup", "WeightDist",
+    "build_problem", "degrade", "fail_and_prune", "PruneMap", "gen_congested", "gen_transit", "gen_uncongested", "group_streams", "problem_from_arrays", "read_problem", "validate", "write_problem",
     "PmpSolver", "Solution", "SolverConfig", "SolverState", "SolveStatus", "TraceRecord", "WarmStart",
     "check_termination", "objective", "recover_duals", "to_string", "update_rho",
     "TransitReportRow", "normalized_route_prices", "transit_report", "write_trace_csv", "write_transit_report_csv",

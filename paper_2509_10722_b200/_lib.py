@@ -124,6 +124,7 @@ SIGNATURES = {
     "numpmp_gpu_set_state": (C.c_int, [P, P, P, P, P, D, I64]),
     "numpmp_gpu_get_state": (C.c_int, [P, P, P, P, P, PD, PI64, P]),
     "numpmp_gpu_step": (C.c_int, [P, PD, PD]),
+    "numpmp_gpu_residuals": (C.c_int, [P, P, P, P, D, PD, PD]),
     "numpmp_gpu_run": (C.c_int, [P, P, P, P, P, C.POINTER(SolutionInfo), P, I64]),
     "numpmp_gpu_run_device": (C.c_int, [P, C.POINTER(SolutionInfo)]),
     "numpmp_gpu_export_layout": (C.c_int, [P, P, P, P]),

@@ -246,6 +246,31 @@ __global__ void k_sum_parts(const double* __restrict__ part, int count, double* 
 
 __global__ void k_start_clock(Ctrl* c) { c->t0_ns = globaltimer_ns(); }
 
+// residuals() (solver.hpp:139-154) on terminal-space device arrays: per-CTA
+// partials of r^2 = sum_l |l| pbar_l^2 (|l| = deg + 1) and
+// s^2 = sum_t (rho (z_t - z'_t))^2 over a fixed grid-stride mapping, summed
+// in CTA order by k_sum_parts.  Launched with the same shape on every call,
+// so the result is a function of the arrays alone: numpmp_gpu_step returns
+// exactly what numpmp_gpu_residuals computes from the states it issued.
+constexpr int kResidualGrid = 4 * 148;
+__global__ void __launch_bounds__(kThreads) k_residual_parts(const double* __restrict__ pbar,
+                                                             const int* __restrict__ deg, long long m,
+                                                             const double* __restrict__ z,
+                                                             const double* __restrict__ zp, long long J,
+                                                             double rho, double* __restrict__ part) {
+  double v[2] = {0.0, 0.0};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < m; l += stride) {
+    const double pb = pbar[l];
+    v[0] += static_cast<double>(deg[l] + 1) * pb * pb;
+  }
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < J; t += stride) {
+    const double d = rho * (z[t] - zp[t]);
+    v[1] += d * d;
+  }
+  block_sum_store<2>(v, part + 2 * blockIdx.x);
+}
+
 // ---------------------------------------------- warm-start recipes (warm.hpp)
 // ratio_l = c_after / c_before; price_l = lambda_raw_l / ratio_l (warm.hpp:29-51).
 __global__ void k_degrade_links(const double* __restrict__ cap_after, long long m,

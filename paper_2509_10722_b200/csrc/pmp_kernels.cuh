@@ -703,10 +703,19 @@ __device__ __forceinline__ double link_epilogue(const IterArgs& a, long long r, 
   return link_update(a, r, L, d, load_link(a, r, pol), rho, part, pol_last, Bn_out, prn_out);
 }
 
+// 1.0 when this device's run has exceeded the time limit (solver.hpp:466-473).
+__device__ __forceinline__ double time_over_flag(const IterArgs& a) {
+  return (a.time_limit_ns > 0 && globaltimer_ns() - a.ctrl->t0_ns > a.time_limit_ns) ? 1.0 : 0.0;
+}
+
 // Finalize one iteration on the device: r, s, then the exact control order
-// of PmpSolver::run (solver.hpp:450-476).  Runs on one thread.
+// of PmpSolver::run (solver.hpp:450-476).  Runs on one thread.  over_time:
+// < 0 reads this device's clock; >= 0 is the sum of the ranks' time_over_flag
+// exchanged with the residual partials, so every rank of a sharded run stops
+// at the same iteration (a rank's own clock would let them disagree).
 __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, double obj,
-                                   double r2, double cross, double ddb2, double dzs2) {
+                                   double r2, double cross, double ddb2, double dzs2,
+                                   double over_time = -1.0) {
   Ctrl* c = a.ctrl;
   double s2r = tda2 - 2.0 * cross + ddb2 + dzs2;
   if (s2r < 0.0) s2r = 0.0;  // rounding of the expanded form near zero
@@ -739,7 +748,7 @@ __device__ void finalize_iteration(const IterArgs& a, double rho, double tda2, d
     row.objective = obj;
     a.trace[c->trace_len++] = row;
   }
-  if (a.time_limit_ns > 0 && globaltimer_ns() - c->t0_ns > a.time_limit_ns) {
+  if (over_time < 0.0 ? time_over_flag(a) > 0.0 : over_time > 0.0) {
     c->status = ST_TIMELIMIT;
     c->done = 1;
     return;
@@ -810,7 +819,8 @@ __device__ __forceinline__ void last_block_finalize(const IterArgs& a, double rh
   if (wib < 6 && lane == 0) sums[wib] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
-    finalize_iteration(a, rho, sums[0], sums[1], sums[2], sums[3], sums[4], sums[5]);
+    finalize_iteration(a, rho, sums[0], sums[1], sums[2], sums[3], sums[4], sums[5],
+                       scalars_in_lbuf ? __ldcg(a.Lbuf + a.m + 2) : -1.0);
     a.ctrl->ticket = 0;
     __threadfence();
   }
@@ -822,8 +832,8 @@ __device__ __forceinline__ void last_block_finalize(const IterArgs& a, double rh
 //   LP_FUSED  : last block, single GPU: L = Lacc + partial, link epilogue,
 //               residual partials, last-CTA finalize.
 //   LP_GATHER : last block, sharded: local loads -> Lbuf; the last CTA folds
-//               the stream-pass scalars into Lbuf[m], Lbuf[m+1] (one NCCL
-//               all-reduce carries both).
+//               the stream-pass scalars into Lbuf[m], Lbuf[m+1] and its
+//               time-limit flag into Lbuf[m+2] (one NCCL all-reduce carries all).
 //   LP_ROWSUM : last block, outside the iteration: L -> out (R src).
 //   LP_P2P    : last block, peer-memory exchange: the row's local load is
 //               stored straight into the owning rank's slot for this rank
@@ -995,6 +1005,7 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
     if (threadIdx.x == 0) {
       a.Lbuf[a.m] = k1s[0];
       a.Lbuf[a.m + 1] = k1s[1];
+      a.Lbuf[a.m + 2] = time_over_flag(a);  // summed by the all-reduce
       a.ctrl->ticket2 = 0;
     }
     return;

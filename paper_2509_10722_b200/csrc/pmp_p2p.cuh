@@ -138,10 +138,13 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
   __shared__ double eps[4];
   multi_sum(p.ep_part, gridDim.x, 4, 4, eps);
   if (threadIdx.x == 0) {
-    const double row[6] = {__ldcg(p.k1_scalars), __ldcg(p.k1_scalars + 1), eps[0], eps[1], eps[2], eps[3]};
+    // the residual partials and this rank's time-limit flag (finalize sums
+    // the flags, so every rank takes the same TimeLimit decision)
+    const double row[7] = {__ldcg(p.k1_scalars), __ldcg(p.k1_scalars + 1), eps[0], eps[1], eps[2], eps[3],
+                           time_over_flag(a)};
     for (int q = 0; q < p.world; ++q) {
       double* xs = ld_ptr(p.xs_peer + q) + 8 * p.rank;
-      for (int i = 0; i < 6; ++i) xs[i] = row[i];
+      for (int i = 0; i < 7; ++i) xs[i] = row[i];
     }
     a.ctrl->ticket3 = 0;
     p2p_signal_all(p, 1);
@@ -154,11 +157,11 @@ __global__ void k_p2p_finalize(IterArgs a) {
   const double rho = a.ctrl->rho;
   const P2PArgs& p = a.p2p;
   p2p_wait_counter(p, 1);
-  double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double s[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double* xs = ld_ptr(p.xs_peer + p.rank);
   for (int q = 0; q < p.world; ++q)
-    for (int i = 0; i < 6; ++i) s[i] += __ldcg(xs + 8 * q + i);
-  finalize_iteration(a, rho, s[0], s[1], s[2], s[3], s[4], s[5]);
+    for (int i = 0; i < 7; ++i) s[i] += __ldcg(xs + 8 * q + i);
+  finalize_iteration(a, rho, s[0], s[1], s[2], s[3], s[4], s[5], s[6]);
 }
 
 // ------------------------------------------------- collectives (setup/post)

@@ -121,25 +121,75 @@ PinnedCtrlPool& ctrl_pool() {
   return *pool;
 }
 
-// Device memory comes from the device's stream-ordered pool, which is told
-// to keep freed memory reserved: creating and destroying solver handles
-// (e2e steps, warm re-solves) then costs no cudaMalloc/cudaFree round trips.
-void keep_pool_memory(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+// Device memory comes from a stream-ordered pool private to this library
+// (one per device, created on first use) that keeps freed memory reserved:
+// creating and destroying solver handles (e2e steps, warm re-solves) then
+// costs no cudaMalloc/cudaFree round trips, and the device's default pool --
+// which other CUDA code in the host process may use -- is left untouched.
+cudaMemPool_t lib_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
     uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[device] = p;
   }
-  done[device] = true;
+  return pools[device];
+}
+
+// cudaMallocAsync from the library pool of the stream's current device.
+cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool = lib_pool(dev);
+  if (!pool) return cudaMallocAsync(p, bytes, stream);
+  return cudaMallocFromPoolAsync(p, bytes, pool, stream);
+}
+
+// The device-wide persisting-L2 limit is raised for the handles' lifetime
+// and restored to the caller's value when the last handle on the device is
+// destroyed.
+struct L2LimitGuard {
+  std::mutex mu;
+  int users[64] = {};
+  size_t saved[64] = {};
+  void acquire(int device, size_t want) {
+    if (device < 0 || device >= 64 || want == 0) return;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t cur = 0;
+    if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) return;
+    if (users[device]++ == 0) saved[device] = cur;
+    int dev_max = 0;
+    cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxPersistingL2CacheSize, device);
+    const size_t set = std::min<size_t>(want, static_cast<size_t>(dev_max));
+    if (cur != set) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set);
+  }
+  void release(int device) {
+    if (device < 0 || device >= 64) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (users[device] == 0 || --users[device] > 0) return;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, saved[device]);
+  }
+};
+L2LimitGuard& l2_guard() {
+  static L2LimitGuard* g = new L2LimitGuard();
+  return *g;
 }
 
 template <class T>
 T* dalloc(size_t count, int64_t* bytes, cudaStream_t stream) {
   T* p = nullptr;
   const size_t b = sizeof(T) * (count > 0 ? count : 1);
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&p), b, stream));
+  CK(lib_malloc_async(reinterpret_cast<void**>(&p), b, stream));
   *bytes += static_cast<int64_t>(b);
   return p;
 }
@@ -210,6 +260,12 @@ struct numpmp_gpu {
   double* ep_part = nullptr;
   double* k1_scalars = nullptr;
   int64_t dev_bytes = 0;
+  bool l2_guard_held = false;  // holds a reference on the device's persisting-L2 limit
+  // get_state fingerprint: set_state of exactly the state the handle last
+  // issued (nothing ran since) keeps the device state instead of
+  // re-decomposing z on the host
+  uint64_t issued_fp = 0;
+  bool issued_valid = false;
 
   // problem
   int* col_ptr = nullptr;
@@ -231,7 +287,7 @@ struct numpmp_gpu {
   double* v_alt[2] = {nullptr, nullptr};  // v for rho*gamma, rho/gamma (rho-update iterations)
   double* ps0 = nullptr;    // slack flows of an uploaded state
   double* pbar0 = nullptr;  // link averages of an uploaded state
-  double* Lbuf = nullptr;   // m + 2
+  double* Lbuf = nullptr;   // m + 3 (sharded: loads, stream-pass scalars, time-limit flag)
   double* Lacc = nullptr;   // m: link loads accumulated over the column blocks
   double* k1_part = nullptr;
   double* k2_part = nullptr;
@@ -480,7 +536,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     k_p2p_finalize<<<1, 32, 0, h->stream>>>(a);
     mark(2);
   } else if (h->sharded) {
-    NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 2), ncclDouble, ncclSum, h->comm,
+    NK(AllReduce(h->Lbuf, h->Lbuf, static_cast<size_t>(h->m + 3), ncclDouble, ncclSum, h->comm,
                  h->stream));
     k_link_epilogue<0><<<h->grid3, kThreads, 0, h->stream>>>(a);
     mark(2);
@@ -640,7 +696,7 @@ void build_csr(numpmp_gpu* h, int64_t s0, int64_t s1, int* row_ptr_out, int* col
     size_t temp_bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, h->row_idx + t0, keys_out, vals_in,
                                        vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
-    CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
+    CK(lib_malloc_async(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
     CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, h->row_idx + t0, keys_out, vals_in,
                                        vals_out, static_cast<int>(nnz), 0, end_bit, h->stream));
     k_row_ptr_from_sorted<<<grid_for(nnz + 1), 256, 0, h->stream>>>(keys_out, nnz, h->m,
@@ -721,7 +777,7 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, nseg, row_vstart, static_cast<int>(m + 1),
                                    h->stream));
   void* temp = nullptr;
-  CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
+  CK(lib_malloc_async(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
   CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nseg, row_vstart, static_cast<int>(m + 1),
                                    h->stream));
   std::vector<int> vstart(static_cast<size_t>(m) + 1);
@@ -805,7 +861,6 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   PhaseTimer pt;
   CK(cudaSetDevice(h->device));
-  keep_pool_memory(h->device);
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
   for (cudaEvent_t& e : h->pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -814,16 +869,13 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   // L2 set-aside for the evict_last lines (x of the live column blocks, v):
   // 32 MB measured best at config C (profiles/r1_l2_sweep.txt);
   // NUMPMP_L2_PERSIST_MB overrides (0 = leave the device limit alone).
+  // Restored when the last handle on the device is destroyed.
   {
     size_t want = size_t(32) << 20;
     if (const char* env = std::getenv("NUMPMP_L2_PERSIST_MB")) want = static_cast<size_t>(std::atoll(env)) << 20;
     if (want > 0) {
-      int dev_max = 0;
-      CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxPersistingL2CacheSize, h->device));
-      size_t cur = 0;
-      CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-      const size_t set = std::min<size_t>(want, static_cast<size_t>(dev_max));
-      if (cur != set) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set));
+      l2_guard().acquire(h->device, want);
+      h->l2_guard_held = true;
     }
   }
   pt.mark("create: stream");
@@ -847,7 +899,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   for (int i = 0; i < 2; ++i) h->v_alt[i] = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->ps0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->pbar0 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
-  h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 2, b, h->stream);
+  h->Lbuf = dalloc<double>(static_cast<size_t>(m) + 3, b, h->stream);
   h->Lacc = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->scratch_m = dalloc<double>(static_cast<size_t>(m), b, h->stream);
   h->scratch_m2 = dalloc<double>(static_cast<size_t>(m), b, h->stream);
@@ -861,7 +913,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
 
   // Upload.  Offsets travel as int64 and are narrowed on the device.
   long long* off64 = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&off64), 8 * static_cast<size_t>(n + 1), h->stream));
+  CK(lib_malloc_async(reinterpret_cast<void**>(&off64), 8 * static_cast<size_t>(n + 1), h->stream));
   upload(h, off64, pv->stream_offsets, 8 * static_cast<size_t>(n + 1));
   k_offsets_to_i32<<<grid_for(n + 1), 256, 0, h->stream>>>(off64, h->col_ptr, n + 1);
   CK(cudaGetLastError());
@@ -877,7 +929,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   // (solver.hpp:275-284; no device prox).
   {
     unsigned long long* bad = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&bad), 6 * sizeof(unsigned long long), h->stream));
+    CK(lib_malloc_async(reinterpret_cast<void**>(&bad), 6 * sizeof(unsigned long long), h->stream));
     CK(cudaMemsetAsync(bad, 0, 6 * sizeof(unsigned long long), h->stream));
     k_validate<<<grid_for(std::max(n, m)), 256, 0, h->stream>>>(off64, h->row_idx, h->w, h->kind,
                                                                h->cap, n, m, bad);
@@ -967,6 +1019,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
 }
 
 void reset_ctrl(numpmp_gpu* h, double rho, int64_t iter) {
+  h->issued_valid = false;
   Ctrl c{};
   c.rho = rho;
   c.rho_iter = rho;
@@ -1078,7 +1131,7 @@ void do_warm_after_degrade(numpmp_gpu* h, const double* cap_before, const double
   size_t temp_bytes = 0;
   CK(cub::DeviceReduce::Min(nullptr, temp_bytes, ratio, h->scalars, static_cast<int>(h->m), h->stream));
   void* temp = nullptr;
-  CK(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
+  CK(lib_malloc_async(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
   CK(cub::DeviceReduce::Min(temp, temp_bytes, ratio, h->scalars, static_cast<int>(h->m), h->stream));
   double worst = 1.0;
   CK(cudaMemcpyAsync(&worst, h->scalars, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -1403,6 +1456,11 @@ int numpmp_gpu_set_warm(numpmp_gpu* h, const double* x0, const double* price, do
   GUARD(h, do_set_warm(h, x0, price, rho));
 }
 
+namespace {
+uint64_t state_fingerprint(const double* p, const double* z, const double* p_bar, const double* price,
+                           size_t J, size_t m, double rho, int64_t iter);
+}  // namespace
+
 // Loads an arbitrary terminal-space state.  z is decomposed as
 // z_t = A_j - B_l by a breadth-first walk over each connected component of
 // the stream/link incidence (root link potential B = 0), then verified.
@@ -1415,6 +1473,11 @@ int numpmp_gpu_set_state(numpmp_gpu* h, const double* p, const double* z, const 
       throw GpuError{NUMPMP_INVALID_ARGUMENT, "state arrays must not be null"};
     if (!(rho > 0.0)) throw GpuError{NUMPMP_INVALID_ARGUMENT, "state rho must be > 0"};
     const int64_t n = h->n, m = h->m, nnz = h->nnz;
+    if (h->issued_valid &&
+        state_fingerprint(p, z, p_bar, price, static_cast<size_t>(nnz + m), static_cast<size_t>(m), rho, iter) ==
+            h->issued_fp) {
+      return NUMPMP_OK;  // the state this handle issued last and still holds: nothing to upload
+    }
     std::vector<int> col_ptr(static_cast<size_t>(n) + 1), row_idx(static_cast<size_t>(nnz));
     CK(cudaMemcpy(col_ptr.data(), h->col_ptr, 4 * (n + 1), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(row_idx.data(), h->row_idx, 4 * nnz, cudaMemcpyDeviceToHost));
@@ -1486,44 +1549,102 @@ int numpmp_gpu_set_state(numpmp_gpu* h, const double* p, const double* z, const 
   });
 }
 
+namespace {
+
+// Fingerprint of a terminal-space state (4 independent multiply-xor lanes
+// over the raw 64-bit words): set_state recognises the state get_state
+// issued last.
+uint64_t state_fingerprint(const double* p, const double* z, const double* p_bar, const double* price,
+                           size_t J, size_t m, double rho, int64_t iter) {
+  uint64_t h[4] = {0x243f6a8885a308d3ull, 0x13198a2e03707344ull, 0xa4093822299f31d0ull, 0x082efa98ec4e6c89ull};
+  auto mix = [&](const double* a, size_t n) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(a);
+    size_t i = 0;
+    for (; i + 4 <= n; i += 4)
+      for (int k = 0; k < 4; ++k) h[k] = (h[k] ^ w[i + k]) * 0x100000001b3ull;
+    for (; i < n; ++i) h[0] = (h[0] ^ w[i]) * 0x100000001b3ull;
+    for (int k = 0; k < 4; ++k) h[k] ^= h[k] >> 29;
+  };
+  mix(p, J);
+  mix(z, J);
+  mix(p_bar, m);
+  mix(price, m);
+  mix(&rho, 1);
+  uint64_t it = static_cast<uint64_t>(iter);
+  mix(reinterpret_cast<const double*>(&it), 1);
+  return h[0] ^ (h[1] * 3) ^ (h[2] * 5) ^ (h[3] * 7);
+}
+
+// The current state in terminal space on the device (get_state, step):
+// p / z / prev_z (length J, any may be null) and the device pointers of the
+// slack flows and link averages.
+void materialize_state(numpmp_gpu* h, const Ctrl& c, double* dp, double* dz, double* dzp, double** ps_out,
+                       double** pbar_out) {
+  const int64_t n = h->n, m = h->m, nnz = h->nnz;
+  const int cu = h->cur, pv = h->cur ^ 1;
+  double* ps_d = h->ps0;
+  double* pbar_d = h->pbar0;
+  if (h->iters_since_upload > 0) {
+    // slack flows and averages of the last iteration, same arithmetic
+    global_row_sums(h, h->x, h->scratch_m);
+    k_materialize_links<<<grid_for(m), 256, 0, h->stream>>>(
+        h->scratch_m, h->deg, nullptr, h->cap, h->zs[pv], h->pr[pv], c.rho_iter, m,
+        h->scratch_m2, h->Lbuf);
+    CK(cudaGetLastError());
+    ps_d = h->scratch_m2;
+    pbar_d = h->Lbuf;
+  }
+  if (dp || dz || dzp) {
+    k_expand_terminals<<<grid_for(n), 256, 0, h->stream>>>(
+        h->col_ptr, h->row_idx, n, h->x, h->A[cu], h->B[cu], h->A[pv], h->B[pv], dp, dz, dzp);
+    CK(cudaGetLastError());
+    if (dp) CK(cudaMemcpyAsync(dp + nnz, ps_d, 8 * m, cudaMemcpyDeviceToDevice, h->stream));
+    if (dz) CK(cudaMemcpyAsync(dz + nnz, h->zs[cu], 8 * m, cudaMemcpyDeviceToDevice, h->stream));
+    if (dzp) CK(cudaMemcpyAsync(dzp + nnz, h->zs[pv], 8 * m, cudaMemcpyDeviceToDevice, h->stream));
+  }
+  if (ps_out) *ps_out = ps_d;
+  if (pbar_out) *pbar_out = pbar_d;
+}
+
+// r, s of residuals() (solver.hpp:139-154) from device arrays (k_residual_parts).
+void device_residuals(numpmp_gpu* h, const double* pbar_d, const double* z_d, const double* zp_d, double rho,
+                      double* r_norm, double* s_norm) {
+  double* part = nullptr;
+  CK(lib_malloc_async(reinterpret_cast<void**>(&part), 16 * kResidualGrid, h->stream));
+  k_residual_parts<<<kResidualGrid, kThreads, 0, h->stream>>>(pbar_d, h->deg, h->m, z_d, zp_d, h->nnz + h->m,
+                                                              rho, part);
+  CK(cudaGetLastError());
+  k_sum_parts<<<1, kThreads, 0, h->stream>>>(part, kResidualGrid, h->scalars);
+  CK(cudaGetLastError());
+  double rs[2] = {0.0, 0.0};
+  CK(cudaMemcpyAsync(rs, h->scalars, 16, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFreeAsync(part, h->stream);
+  *r_norm = std::sqrt(rs[0]);
+  *s_norm = std::sqrt(rs[1]);
+}
+
+}  // namespace
+
 int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, double* price,
                          double* rho, int64_t* iter, double* prev_z) {
   GUARD(h, {
     const Ctrl c = read_ctrl(h);
-    const int64_t n = h->n, m = h->m, nnz = h->nnz;
-    const int cu = h->cur, pv = h->cur ^ 1;
+    const int64_t m = h->m, nnz = h->nnz;
     const bool stepped = h->iters_since_upload > 0;
     if (rho) *rho = c.rho;
     if (iter) *iter = c.iter;
-    if (price) download(h, price, h->pr[cu], 8 * static_cast<size_t>(m));
-    double* ps_d = h->ps0;
-    double* pbar_d = h->pbar0;
-    if (stepped) {
-      // slack flows and averages of the last iteration, same arithmetic
-      global_row_sums(h, h->x, h->scratch_m);
-      k_materialize_links<<<grid_for(m), 256, 0, h->stream>>>(
-          h->scratch_m, h->deg, nullptr, h->cap, h->zs[pv], h->pr[pv], c.rho_iter, m,
-          h->scratch_m2, h->Lbuf);
-      CK(cudaGetLastError());
-      ps_d = h->scratch_m2;
-      pbar_d = h->Lbuf;
-    }
+    if (price) download(h, price, h->pr[h->cur], 8 * static_cast<size_t>(m));
     const size_t J = static_cast<size_t>(nnz + m);
     double *dp = nullptr, *dz = nullptr, *dzp = nullptr;
-    if (p || z || prev_z) {
-      if (p) CK(cudaMallocAsync(reinterpret_cast<void**>(&dp), 8 * J, h->stream));
-      if (z) CK(cudaMallocAsync(reinterpret_cast<void**>(&dz), 8 * J, h->stream));
-      if (prev_z) CK(cudaMallocAsync(reinterpret_cast<void**>(&dzp), 8 * J, h->stream));
-      k_expand_terminals<<<grid_for(n), 256, 0, h->stream>>>(
-          h->col_ptr, h->row_idx, n, h->x, h->A[cu], h->B[cu], h->A[pv], h->B[pv], dp, dz, dzp);
-      CK(cudaGetLastError());
-      if (dp) CK(cudaMemcpyAsync(dp + nnz, ps_d, 8 * m, cudaMemcpyDeviceToDevice, h->stream));
-      if (dz) CK(cudaMemcpyAsync(dz + nnz, h->zs[cu], 8 * m, cudaMemcpyDeviceToDevice, h->stream));
-      if (dzp) CK(cudaMemcpyAsync(dzp + nnz, h->zs[pv], 8 * m, cudaMemcpyDeviceToDevice, h->stream));
-      if (p) download(h, p, dp, 8 * J);
-      if (z) download(h, z, dz, 8 * J);
-      if (prev_z) download(h, prev_z, dzp, 8 * J);
-    }
+    if (p) CK(lib_malloc_async(reinterpret_cast<void**>(&dp), 8 * J, h->stream));
+    if (z) CK(lib_malloc_async(reinterpret_cast<void**>(&dz), 8 * J, h->stream));
+    if (prev_z) CK(lib_malloc_async(reinterpret_cast<void**>(&dzp), 8 * J, h->stream));
+    double* pbar_d = nullptr;
+    materialize_state(h, c, dp, dz, dzp, nullptr, &pbar_d);
+    if (p) download(h, p, dp, 8 * J);
+    if (z) download(h, z, dz, 8 * J);
+    if (prev_z) download(h, prev_z, dzp, 8 * J);
     if (p_bar) download(h, p_bar, pbar_d, 8 * static_cast<size_t>(m));
     CK(cudaStreamSynchronize(h->stream));
     cudaFreeAsync(dp, h->stream);
@@ -1533,18 +1654,74 @@ int numpmp_gpu_get_state(numpmp_gpu* h, double* p, double* z, double* p_bar, dou
       if (p) std::memcpy(p, h->host_p.data(), 8 * J);
       if (p_bar) std::memcpy(p_bar, h->host_pbar.data(), 8 * static_cast<size_t>(m));
     }
+    h->issued_valid = false;
+    if (p && z && p_bar && price && !h->sharded) {
+      h->issued_fp = state_fingerprint(p, z, p_bar, price, J, static_cast<size_t>(m), c.rho, c.iter);
+      h->issued_valid = true;
+    }
+  });
+}
+
+// Replaces residuals(state, prev, layout) (solver.hpp:139-154) with the
+// device reduction numpmp_gpu_step uses.
+int numpmp_gpu_residuals(numpmp_gpu* h, const double* p_bar, const double* z, const double* prev_z,
+                         double rho, double* r_norm, double* s_norm) {
+  GUARD(h, {
+    if (h->sharded) throw GpuError{NUMPMP_INVALID_ARGUMENT, "residuals is not supported on sharded handles"};
+    if (!p_bar || !z || !prev_z || !r_norm || !s_norm)
+      throw GpuError{NUMPMP_INVALID_ARGUMENT, "residuals: arrays must not be null"};
+    const size_t J = static_cast<size_t>(h->nnz + h->m), mb = 8 * static_cast<size_t>(h->m);
+    double *dpb = nullptr, *dz = nullptr, *dzp = nullptr;
+    CK(lib_malloc_async(reinterpret_cast<void**>(&dpb), mb, h->stream));
+    CK(lib_malloc_async(reinterpret_cast<void**>(&dz), 8 * J, h->stream));
+    CK(lib_malloc_async(reinterpret_cast<void**>(&dzp), 8 * J, h->stream));
+    upload(h, dpb, p_bar, mb);
+    upload(h, dz, z, 8 * J);
+    upload(h, dzp, prev_z, 8 * J);
+    device_residuals(h, dpb, dz, dzp, rho, r_norm, s_norm);
+    cudaFreeAsync(dpb, h->stream);
+    cudaFreeAsync(dz, h->stream);
+    cudaFreeAsync(dzp, h->stream);
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 
 int numpmp_gpu_step(numpmp_gpu* h, double* r_norm, double* s_norm) {
   GUARD(h, {
+    h->issued_valid = false;
+    {  // a previous run left `done` set: clear the run control (as run_loop does)
+      Ctrl c = read_ctrl(h);
+      c.run_k = 0;
+      c.done = 0;
+      c.status = ST_RUNNING;
+      c.ticket = 0;
+      c.ticket2 = 0;
+      c.ticket3 = 0;
+      std::memcpy(&h->ctrl_host[1], &c, sizeof(Ctrl));
+      CK(cudaMemcpyAsync(h->ctrl, &h->ctrl_host[1], sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+    }
     enqueue_iteration(h, h->cur, MODE_STEP, nullptr, false);
     if (h->p2p) p2p_sync_link_state(h);
     const Ctrl c = read_ctrl(h);
     h->cur ^= 1;
     h->iters_since_upload += 1;
-    if (r_norm) *r_norm = c.r_norm;
-    if (s_norm) *s_norm = c.s_norm;
+    double r = c.r_norm, s = c.s_norm;
+    if (!h->sharded) {
+      // step() returns residuals(after, before) (solver.hpp:316-318): the
+      // direct terminal-space form on the materialised states, the same
+      // reduction numpmp_gpu_residuals runs on host copies of them
+      const size_t J = static_cast<size_t>(h->nnz + h->m);
+      double *dz = nullptr, *dzp = nullptr, *pbar_d = nullptr;
+      CK(lib_malloc_async(reinterpret_cast<void**>(&dz), 8 * J, h->stream));
+      CK(lib_malloc_async(reinterpret_cast<void**>(&dzp), 8 * J, h->stream));
+      materialize_state(h, c, nullptr, dz, dzp, nullptr, &pbar_d);
+      device_residuals(h, pbar_d, dz, dzp, c.rho_iter, &r, &s);
+      cudaFreeAsync(dz, h->stream);
+      cudaFreeAsync(dzp, h->stream);
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    if (r_norm) *r_norm = r;
+    if (s_norm) *s_norm = s;
   });
 }
 
@@ -1557,6 +1734,7 @@ namespace {
 // the device set `done` exit at entry.
 void run_loop(numpmp_gpu* h) {
   PhaseTimer pt;
+  h->issued_valid = false;
   const int start = h->cur;
   const int lpi = h->launches_per_iteration();
   const size_t set_size = static_cast<size_t>(kBatchIters * lpi + 1);
@@ -1831,6 +2009,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   PhaseTimer pt;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->l2_guard_held) l2_guard().release(h->device);
   for (void* base : h->peer_bases) cudaIpcCloseMemHandle(base);
   if (h->xregion) {
     cudaFree(h->xregion);

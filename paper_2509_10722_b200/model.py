@@ -152,6 +152,39 @@ def build_problem(streams: Sequence[Stream], capacities: Sequence[float]) -> Pro
 
 
 # ---------------------------------------------------------------- generators
+@dataclass
+class TypeGroup:  # model.hpp:243-253
+    kind: StreamKind
+    extension: str
+    tau: int
+    members: np.ndarray         # stream ids, ascending
+    weights: np.ndarray
+    terminal_links: np.ndarray  # [tau][len(members)]: link of terminal i of member k
+
+
+def group_streams(problem: Problem) -> List[TypeGroup]:
+    """model.hpp:255-286: streams partitioned by (tau, kind), ordered by
+    ascending tau, then kind, then first member (the extension name is part
+    of the key only for Extension streams, which this package rejects)."""
+    so = np.asarray(problem.stream_offsets, np.int64)
+    tau = np.diff(so)
+    kinds = np.asarray(problem.kinds, np.int64)
+    key = tau * 8 + kinds
+    order = np.lexsort((np.arange(problem.n), key))  # stable: members ascending within a key
+    out = []
+    if problem.n == 0:
+        return out
+    ks = key[order]
+    cuts = np.flatnonzero(np.diff(ks)) + 1
+    for seg in np.split(order, cuts):
+        t = int(tau[seg[0]])
+        links = problem.route_links[(so[seg][:, None] + np.arange(t)[None, :]).reshape(-1)].reshape(len(seg), t)
+        out.append(TypeGroup(StreamKind(int(kinds[seg[0]])), "", t, seg.astype(np.int64),
+                             np.asarray(problem.weights, np.float64)[seg], np.ascontiguousarray(links.T)))
+    out.sort(key=lambda g: (g.tau, int(g.kind), int(g.members[0])))
+    return out
+
+
 class GenKind(IntEnum):  # gen.hpp:18
     Log = 0
     Linear = 1

@@ -5,14 +5,14 @@ nonzeros; every rank holds its streams' CSC and a local CSR over all m
 links.  Two exchanges are available for the per-iteration sum of the
 partial link loads R_g x_g:
 
-* ``exchange="p2p"`` (default): the fused peer-memory exchange of
+* ``exchange="p2p"`` (bench.py's default; pass it explicitly): the fused peer-memory exchange of
   csrc/pmp_p2p.cuh.  Links are owned in contiguous ranges; the link pass
   stores each row's partial load straight into the owner's HBM over NVLink
   (overlapped with the remaining gathers), the owner runs the link epilogue
   for its links only and stores v into every rank's HBM, and all ranks sum
   the same per-rank residual partials in rank order, so they take the same
   termination and rho decisions.  No NCCL kernel sits in the loop.
-* ``exchange="nccl"``: replicated link state, one NCCL all-reduce of the m
+* ``exchange="nccl"`` (the constructor's default): replicated link state, one NCCL all-reduce of the m
   partial loads (+2 scalars) inside the device graph, replicated epilogue.
   Kept as the library baseline the fused path is measured against.
 
@@ -158,10 +158,15 @@ class ShardedPmpSolver:
         if warm is None:
             rc = L.numpmp_gpu_set_cold(self._h)
         else:
-            x0 = np.ascontiguousarray(np.asarray(warm.x0, np.float64)[self.stream_begin:self.stream_begin + p.n])
-            if x0.shape[0] != p.n:
+            xg = np.asarray(warm.x0, np.float64)
+            if xg.shape[0] != self.full.n:
                 raise ValueError("warm start: x0 length does not match n")
-            price = None if warm.price is None else np.ascontiguousarray(warm.price, np.float64)
+            x0 = np.ascontiguousarray(xg[self.stream_begin:self.stream_begin + p.n])
+            price = None
+            if warm.price is not None and len(warm.price) > 0:  # empty: start prices at zero (solver.hpp:101-105)
+                price = np.ascontiguousarray(warm.price, np.float64)
+                if price.shape[0] != p.m:
+                    raise ValueError("warm start: price length mismatch")
             rc = L.numpmp_gpu_set_warm(self._h, _lib.ptr(x0), _lib.ptr(price), float(warm.rho))
         if rc:
             raise_for(rc, L.numpmp_gpu_last_error(self._h).decode())

@@ -139,6 +139,7 @@ class PmpSolver:
             raise_for(rc, L.numpmp_gpu_last_error(None).decode())
         self._h = h
         self._final: Optional[Tuple[SolverState, np.ndarray]] = None
+        self._groups = None
 
     # solver.hpp:289-291
     def problem(self) -> Problem:
@@ -213,6 +214,32 @@ class PmpSolver:
         state.p, state.z, state.p_bar, state.price = new.p, new.z, new.p_bar, new.price
         state.rho, state.iter = new.rho, new.iter
         return r.value, s.value
+
+    def residuals(self, state: SolverState, prev: SolverState) -> Tuple[float, float]:
+        """residuals(state, prev, layout) (solver.hpp:139-154) on the device:
+        the reduction step() uses, so step() returns exactly
+        ``residuals(after, before)`` for the states it issued."""
+        p = self._problem
+        J = p.nnz + p.m
+        pb = np.ascontiguousarray(state.p_bar, np.float64)
+        z = np.ascontiguousarray(state.z, np.float64)
+        zp = np.ascontiguousarray(prev.z, np.float64)
+        if pb.shape[0] != p.m or z.shape[0] != J or zp.shape[0] != J:
+            raise ValueError("residuals: state arrays do not fit the problem")
+        r, s = C.c_double(), C.c_double()
+        _check(self._h, _lib.lib().numpmp_gpu_residuals(self._h, _lib.ptr(pb), _lib.ptr(z), _lib.ptr(zp),
+                                                        float(state.rho), C.byref(r), C.byref(s)))
+        return r.value, s.value
+
+    def groups(self):
+        """solver.hpp:291 groups(): group_streams of the problem (model.hpp:246-286).
+        The device engine does not batch by group; this is the reference's
+        partition, for callers that inspect it."""
+        if self._groups is None:
+            from .model import group_streams
+
+            self._groups = group_streams(self._problem)
+        return self._groups
 
     # ------------------------------------------- warm-start recipes (warm.hpp)
     def warm_start_after_degrade(self, before: "Problem", prior: Solution) -> WarmStart:

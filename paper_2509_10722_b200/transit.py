@@ -52,15 +52,16 @@ def transit_report(problem: Problem, x, lam, meta: TransitMetadata, od: int, t0:
     """transit.hpp:342-374.  pi: the path prices if already computed; else the
     solver's device path_prices when `solver` is given; else the selected
     streams' route sums in route order (the same bits as path_prices)."""
+    # std::invalid_argument in the reference (transit.hpp:292,343,349) -> ValueError
     if len(meta.stream_od) != problem.n:
-        raise ValidationError("transit report: metadata does not match problem")
+        raise ValueError("transit report: metadata does not match problem")
     k = len(meta.od_origin)
     if od < 0 or od >= k:
-        raise ValidationError(f"unknown OD id {od}; available: 0..{k - 1}")
+        raise ValueError(f"unknown OD id {od}; available: 0..{k - 1}")
     selected = np.flatnonzero((meta.stream_od == od) & (meta.stream_t0 == t0)).tolist()
     lam = np.asarray(lam, np.float64)
     if lam.shape[0] != problem.m:
-        raise ValidationError("path_prices: lambda length mismatch")
+        raise ValueError("path_prices: lambda length mismatch")
     hats = normalized_route_prices(problem, lam, selected)
     if pi is None and solver is not None:
         pi = solver.path_prices(lam)

@@ -185,6 +185,95 @@ int main() {
               max_rel(c.x, a.x) <= 1e-6,
           buf);
   }
+  {  // StepResidualsMatchFreeFunction (test_solver.cpp:245-262): step() ==
+     // the drop-in's residuals() bit for bit; the reference's host
+     // residuals() on the same downloaded states within 1e-12 relative
+    GenSpec spec;
+    spec.m = 40;
+    spec.n = 20;
+    spec.avg_links_per_stream = 4.0;
+    spec.kind = GenKind::Mixed;
+    spec.seed = 9;
+    Problem p = gen_uncongested(spec);
+    gpu::PmpSolver solver(p, SolverConfig{});
+    const gpu::PmpSolver& cs = solver;  // every member the reference declares const, through a const&
+    SolverState st = cs.cold_state();
+    bool bit = true, close = true;
+    for (int iter = 0; iter < 20; ++iter) {
+      SolverState prev = st;
+      auto [r, s] = solver.step(st);
+      auto [r_dev, s_dev] = cs.residuals(st, prev);
+      auto [r_host, s_host] = residuals(st, prev, p.layout);
+      bit = bit && r == r_dev && s == s_dev;
+      close = close && std::fabs(r - r_host) <= 1e-12 * std::max(1.0, r_host) &&
+              std::fabs(s - s_host) <= 1e-12 * std::max(1.0, s_host);
+    }
+    check(bit, "step() == residuals(after, before) bit for bit (20 steps)");
+    check(close, "step() == host residuals() within 1e-12 (20 steps)");
+    // groups() is the reference's partition (model.hpp:255-286)
+    const auto& g = cs.groups();
+    const auto ref_g = group_streams(p);
+    bool same = g.size() == ref_g.size();
+    for (std::size_t i = 0; same && i < g.size(); ++i)
+      same = g[i].tau == ref_g[i].tau && g[i].kind == ref_g[i].kind && g[i].members == ref_g[i].members &&
+             g[i].terminal_links == ref_g[i].terminal_links;
+    check(same && cs.problem().n == p.n && cs.config().alpha == SolverConfig{}.alpha, "const accessors, groups()");
+    WarmStart w;
+    w.x0.assign(static_cast<std::size_t>(p.n), 1.0);
+    const SolverState ws = cs.warm_state(w);
+    PmpSolver cpu(p, SolverConfig{});
+    const SolverState wr = cpu.warm_state(w);
+    check(max_rel(ws.z, wr.z) <= 1e-12 && max_rel(ws.p_bar, wr.p_bar) <= 1e-12, "warm_state() const");
+    solver.solve();
+    const SolverState& fs = cs.final_state();
+    const std::vector<double>& fz = cs.final_prev_z();
+    check(fs.z.size() == fz.size() && fs.iter > 0, "final_state() / final_prev_z() const");
+  }
+  {  // multi-device drop-in: two stream shards with the peer-memory exchange
+     // (both on device 0 here: one host thread per rank, as with 2 GPUs)
+    GenSpec b;
+    b.m = 2000;
+    b.n = 4000;
+    b.avg_links_per_stream = 6.0;
+    b.kind = GenKind::Mixed;
+    b.weights = WeightDist::uniform(0.5, 1.5);
+    b.seed = 11;
+    Problem p = gen_uncongested(b);
+    SolverConfig cfg;
+    cfg.eps_abs = 1e-5;
+    cfg.rho0 = 1000.0;
+    PmpSolver cpu(p, cfg);
+    Solution a = cpu.solve();
+    for (int world : {2, 3}) {
+      gpu::PmpSolver dev(p, cfg, nullptr, std::vector<int>(static_cast<std::size_t>(world), 0));
+      Solution c = dev.solve();
+      Solution c2 = dev.solve();  // repeated solves on the same sharded handles
+      char buf[240];
+      std::snprintf(buf, sizeof buf,
+                    "sharded drop-in (%d ranks, p2p): iterations cpu %lld gpu %lld, x rel %.2e, price rel %.2e",
+                    world, (long long)a.iterations, (long long)c.iterations, max_rel(c.x, a.x),
+                    max_rel(c.lambda_raw, a.lambda_raw));
+      check(a.iterations == c.iterations && a.status == c.status && max_rel(c.x, a.x) <= 1e-6 &&
+                max_rel(c.lambda_raw, a.lambda_raw) <= 1e-6 && c2.x == c.x && c2.iterations == c.iterations &&
+                dev.shard_bounds().size() == static_cast<std::size_t>(world) + 1,
+            buf);
+      bool threw = false;
+      try {
+        dev.cold_state();
+      } catch (const std::logic_error&) {
+        threw = true;
+      }
+      check(threw, "sharded drop-in: terminal-space members throw std::logic_error");
+      WarmStart w;
+      w.x0 = a.x;
+      w.price = a.lambda_raw;
+      w.rho = a.rho_final;
+      Solution d = dev.solve(w);
+      std::snprintf(buf, sizeof buf, "sharded drop-in (%d ranks): warm start from the optimum, %lld iterations",
+                    world, (long long)d.iterations);
+      check(d.iterations <= 5 && d.status == SolveStatus::Converged, buf);
+    }
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -368,11 +368,12 @@ def test_transit_report_errors(reference, tmp_path):
     p, meta = pmp.gen_transit(pmp.TransitSpec(*args), with_meta=True)
     k = len(meta.od_origin)
     x, lam = np.ones(p.n), np.zeros(p.m)
-    with pytest.raises(pmp.ValidationError, match=rf"^unknown OD id {k}; available: 0\.\.{k - 1}$"):
+    # std::invalid_argument in the reference (transit.hpp:343,349) -> ValueError
+    with pytest.raises(ValueError, match=rf"^unknown OD id {k}; available: 0\.\.{k - 1}$"):
         pmp.transit_report(p, x, lam, meta, k, 0)
     with pytest.raises(RuntimeError, match=rf"unknown OD id {k}; available: 0\.\.{k - 1}$"):
         reference.gen_transit(*args).transit_report(x, lam, k, 0, str(tmp_path / "r.csv"))
-    with pytest.raises(pmp.ValidationError, match="metadata does not match problem"):
+    with pytest.raises(ValueError, match="metadata does not match problem"):
         q = pmp.gen_uncongested(_spec(40, 20, 4.0, 2, ("constant", 1.0, 1.0), 9))
         pmp.transit_report(q, np.ones(q.n), np.zeros(q.m), meta, 0, 0)
     # all prices zero: normalized prices are 0 (transit.hpp:318-320)
@@ -477,3 +478,21 @@ def test_bench_reference_arm_is_the_reference_alone():
     assert line["config"] == bench.bench_config("A", 1000, 10000, 49795)
     assert line["iterations_per_step"] == [423]  # config A converges inside the sample
     assert line["cpu_baseline"]["kind"] == "reference"
+
+
+def test_group_streams_matches_reference(reference):
+    # model.hpp:255-286: (tau, kind) partition, ordered by tau, kind, first member
+    for args in [(100, 50, 5.0, 2, ("uniform", 0.5, 1.5), 1), (300, 900, 4.0, 2, ("uniform", 0.5, 1.5), 31),
+                 (1000, 10000, 5.0, 0, ("constant", 1.0, 1.0), 7)]:
+        rp = reference.gen(*args)
+        a = rp.arrays()
+        p = pmp.problem_from_arrays(a.m, a.n, a.capacities, a.weights, a.kinds, a.stream_offsets, a.route_links)
+        got = pmp.group_streams(p)
+        want = rp.groups()
+        assert len(got) == len(want)
+        for g, (tau, kind, members) in zip(got, want):
+            assert (g.tau, int(g.kind)) == (tau, kind)
+            np.testing.assert_array_equal(g.members, members)
+            np.testing.assert_array_equal(g.weights, a.weights[members])
+            for i in range(g.tau):
+                np.testing.assert_array_equal(g.terminal_links[i], a.route_links[a.stream_offsets[members] + i])
