@@ -131,6 +131,8 @@ cudaMemPool_t lib_pool(int device) {
   static cudaMemPool_t pools[64] = {};
   if (device < 0 || device >= 64) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
+  static const char* mode = std::getenv("NUMPMP_POOL");  // A/B: "default" = the device's default pool
+  if (mode && std::strcmp(mode, "default") == 0) return nullptr;
   if (!pools[device]) {
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
@@ -140,6 +142,14 @@ cudaMemPool_t lib_pool(int device) {
     if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (!(mode && std::strcmp(mode, "reuse") == 0)) {
+      // No cross-stream reuse with inserted dependencies: handles of
+      // in-process peer-memory ranks share this pool, and a dependency of one
+      // rank's stream on another's (which may hold a barrier wait) deadlocks.
+      int off = 0;
+      cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &off);
+      cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowOpportunistic, &off);
+    }
     pools[device] = p;
   }
   return pools[device];
@@ -858,9 +868,56 @@ void segment_block(numpmp_gpu* h, ColBlock& cb) {
   cudaFreeAsync(row_vstart, h->stream);
 }
 
+// CUDA loads kernels lazily (CUDA_MODULE_LOADING=LAZY, the CUDA 12
+// default), and loading one may wait for the kernels already running on the
+// device.  Peer-memory ranks in one process spin in barrier kernels while
+// their peers launch kernels, so a first-use load deadlocks them (every
+// wait traps after 60 s).  Every kernel of the library is therefore loaded
+// up front, once per device, before any handle runs.
+template <int kPhase>
+void preload_link_pass(std::vector<const void*>& f) {
+  f.push_back(reinterpret_cast<const void*>(&k_link_pass<kPhase, 0>));
+  f.push_back(reinterpret_cast<const void*>(&k_link_pass<kPhase, 1>));
+  f.push_back(reinterpret_cast<const void*>(&k_link_pass<kPhase, 2>));
+}
+void preload_kernels(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  std::vector<const void*> f;
+#define NUMPMP_K(k) f.push_back(reinterpret_cast<const void*>(&k))
+  NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>);
+  NUMPMP_K(k_link_epilogue<0>); NUMPMP_K(k_link_epilogue<1>);
+  NUMPMP_K(k_refresh_v); NUMPMP_K(k_set_v); NUMPMP_K(k_residual_parts);
+  NUMPMP_K(k_p2p_wait<0>); NUMPMP_K(k_p2p_epilogue); NUMPMP_K(k_p2p_finalize);
+  NUMPMP_K(k_p2p_aux_wait); NUMPMP_K(k_p2p_aux_signal); NUMPMP_K(k_p2p_push_partials);
+  NUMPMP_K(k_p2p_reduce_bcast); NUMPMP_K(k_p2p_push_owned); NUMPMP_K(k_p2p_push_scalars);
+  NUMPMP_K(k_p2p_sum_scalars);
+  NUMPMP_K(k_validate); NUMPMP_K(k_iota); NUMPMP_K(k_degree); NUMPMP_K(k_add_degree); NUMPMP_K(k_max_degree);
+  NUMPMP_K(k_offsets_to_i32); NUMPMP_K(k_gather_i32); NUMPMP_K(k_terminal_stream); NUMPMP_K(k_row_ptr_from_sorted);
+  NUMPMP_K(k_seg_count); NUMPMP_K(k_seg_fill); NUMPMP_K(k_row_sums_seq);
+  NUMPMP_K(k_int_to_double); NUMPMP_K(k_double_to_int);
+  NUMPMP_K(k_materialize_links); NUMPMP_K(k_expand_terminals); NUMPMP_K(k_post_streams); NUMPMP_K(k_post_links);
+  NUMPMP_K(k_sum_parts); NUMPMP_K(k_start_clock); NUMPMP_K(k_warm_links); NUMPMP_K(k_path_prices);
+  NUMPMP_K(k_degrade_links); NUMPMP_K(k_route_min_scale); NUMPMP_K(k_prune_prices); NUMPMP_K(k_recenter_log);
+#undef NUMPMP_K
+  preload_link_pass<LP_ACC>(f);
+  preload_link_pass<LP_FUSED>(f);
+  preload_link_pass<LP_GATHER>(f);
+  preload_link_pass<LP_ROWSUM>(f);
+  preload_link_pass<LP_P2P>(f);
+  for (const void* fn : f) {
+    cudaFuncAttributes attr;
+    CK(cudaFuncGetAttributes(&attr, fn));
+  }
+  done[device] = true;
+}
+
 void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   PhaseTimer pt;
   CK(cudaSetDevice(h->device));
+  preload_kernels(h->device);
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
   for (cudaEvent_t& e : h->pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
