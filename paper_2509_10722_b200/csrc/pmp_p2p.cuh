@@ -23,6 +23,13 @@
 //                        rank takes the same termination / rho decision --
 //                        and runs finalize_iteration.
 //
+// Fused mode (the default when no two ranks share a GPU): the wait and the
+// finalize fold into k_p2p_epilogue<true> -- every CTA's thread 0 acquires
+// "loads stored" itself and the last CTA waits for "epilogue done" and
+// finalizes -- so an iteration is 2 NB + 1 launches, as on one device.
+// Ranks sharing a GPU (the one-GPU test boxes) keep the three launches:
+// there, a spinning CTA could hold the SMs another rank's link pass needs.
+//
 // On rho-update iterations the owner also stores v for both candidate rhos
 // (rho*gamma, rho/gamma) into every rank; finalize_iteration selects one
 // (Ctrl::v_sel), so nothing rebuilds v inside the loop.  Traffic per rank and iteration: 8 (world-1)/world
@@ -55,7 +62,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-__device__ __forceinline__ void p2p_wait_counter(const P2PArgs& p, int which) {
+// Spin until barrier `which` of the current round has every rank's signal.
+// Does not count the round as completed (several CTAs may wait on it).
+__device__ __forceinline__ void p2p_spin_counter(const P2PArgs& p, int which) {
   const unsigned long long target =
       static_cast<unsigned long long>(p.world) * (p.done_cnt[which] + 1);
   const long long t0 = globaltimer_ns();
@@ -63,6 +72,10 @@ __device__ __forceinline__ void p2p_wait_counter(const P2PArgs& p, int which) {
     __nanosleep(64);
     if (globaltimer_ns() - t0 > kP2PTimeoutNs) __trap();
   }
+}
+
+__device__ __forceinline__ void p2p_wait_counter(const P2PArgs& p, int which) {
+  p2p_spin_counter(p, which);
   p.done_cnt[which] += 1;
   __threadfence();
 }
@@ -73,6 +86,17 @@ __device__ __forceinline__ void p2p_signal_all(const P2PArgs& p, int which) {
 }
 
 // ---------------------------------------------------------------- iteration
+// After "epilogue done": the ranks' residual partials in rank order (the
+// same numbers on every rank), then the device finalize.
+__device__ __forceinline__ void p2p_sum_finalize(const IterArgs& a, double rho) {
+  const P2PArgs& p = a.p2p;
+  double s[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const double* xs = ld_ptr(p.xs_peer + p.rank);
+  for (int q = 0; q < p.world; ++q)
+    for (int i = 0; i < 7; ++i) s[i] += __ldcg(xs + 8 * q + i);
+  finalize_iteration(a, rho, s[0], s[1], s[2], s[3], s[4], s[5], s[6]);
+}
+
 template <int kWhich>
 __global__ void k_p2p_wait(IterArgs a) {
   if (threadIdx.x != 0) return;
@@ -80,11 +104,21 @@ __global__ void k_p2p_wait(IterArgs a) {
   p2p_wait_counter(a.p2p, kWhich);
 }
 
-__global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
+// kFused (one GPU per rank): every CTA's thread 0 waits for "loads stored"
+// itself (no k_p2p_wait launch), and the last CTA, after publishing its
+// partials, waits for "epilogue done" and runs the finalize (no
+// k_p2p_finalize launch).  Only valid when no other rank's kernels need this
+// GPU's SMs: a spinning CTA holds its slot.
+template <bool kFused>
+__global__ void __launch_bounds__(kThreads, NUMPMP_EPI_MINB) k_p2p_epilogue(IterArgs a) {
   __shared__ bool s_last;
   if (kernel_should_exit(a.ctrl)) return;
-  const double rho = a.ctrl->rho;
   const P2PArgs& p = a.p2p;
+  if (kFused) {
+    if (threadIdx.x == 0) p2p_spin_counter(p, 0);  // the round is counted by the last CTA
+    __syncthreads();
+  }
+  const double rho = a.ctrl->rho;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
   double part[4] = {0.0, 0.0, 0.0, 0.0};
@@ -128,40 +162,57 @@ __global__ void __launch_bounds__(kThreads) k_p2p_epilogue(IterArgs a) {
     if (has1) finish(l1, L1, d1, in1);
   }
   block_sum_store<4>(part, p.ep_part + 4 * blockIdx.x);  // ends with bar.sync
-  if (threadIdx.x == 0) {  // one cumulative system-scope fence per CTA (grid.sync pattern)
-    __threadfence_system();
+  if (threadIdx.x == 0) {  // one cumulative fence per CTA (grid.sync pattern; scope: see k_link_pass LP_P2P)
+    if (p.cta_sysfence)
+      __threadfence_system();
+    else
+      __threadfence();
     s_last = (atomicAdd(&a.ctrl->ticket3, 1u) == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  __shared__ double eps[4];
-  multi_sum(p.ep_part, gridDim.x, 4, 4, eps);
+  // this rank's six sums, one warp each: the stream passes' (tau dA^2,
+  // objective) and the owner epilogue's four -- the fixed orders of
+  // last_block_finalize
+  static_assert(kWarps >= 6, "one warp per sum");
+  __shared__ double sums[6];
+  {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double v = 0.0;
+    if (wib < 2)
+      v = warp_sum_array(a.k1_part, a.grid1 * a.nblocks, 2, wib, lane);
+    else if (wib < 6)
+      v = warp_sum_array(p.ep_part, gridDim.x, 4, wib - 2, lane);
+    if (wib < 6 && lane == 0) sums[wib] = v;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     // the residual partials and this rank's time-limit flag (finalize sums
     // the flags, so every rank takes the same TimeLimit decision)
-    const double row[7] = {__ldcg(p.k1_scalars), __ldcg(p.k1_scalars + 1), eps[0], eps[1], eps[2], eps[3],
-                           time_over_flag(a)};
+    const double row[7] = {sums[0], sums[1], sums[2], sums[3], sums[4], sums[5], time_over_flag(a)};
     for (int q = 0; q < p.world; ++q) {
       double* xs = ld_ptr(p.xs_peer + q) + 8 * p.rank;
       for (int i = 0; i < 7; ++i) xs[i] = row[i];
     }
     a.ctrl->ticket3 = 0;
+    if (kFused) {
+      p.done_cnt[0] += 1;  // every CTA has passed its wait on barrier 0
+      __threadfence();
+    }
     p2p_signal_all(p, 1);
+    if (kFused) {
+      p2p_wait_counter(p, 1);
+      p2p_sum_finalize(a, rho);
+    }
   }
 }
 
 __global__ void k_p2p_finalize(IterArgs a) {
   if (threadIdx.x != 0) return;
   if (kernel_should_exit(a.ctrl)) return;
-  const double rho = a.ctrl->rho;
-  const P2PArgs& p = a.p2p;
-  p2p_wait_counter(p, 1);
-  double s[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  const double* xs = ld_ptr(p.xs_peer + p.rank);
-  for (int q = 0; q < p.world; ++q)
-    for (int i = 0; i < 7; ++i) s[i] += __ldcg(xs + 8 * q + i);
-  finalize_iteration(a, rho, s[0], s[1], s[2], s[3], s[4], s[5], s[6]);
+  p2p_wait_counter(a.p2p, 1);
+  p2p_sum_finalize(a, a.ctrl->rho);
 }
 
 // ------------------------------------------------- collectives (setup/post)

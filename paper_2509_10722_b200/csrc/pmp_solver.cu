@@ -240,6 +240,8 @@ struct ColBlock {
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
+  int* ix = nullptr;          // interleaved route tiles (k_stream_pass_ix; BlockArgs::ix)
+  unsigned* ix_off = nullptr; // ntiles+1: first row of each tile
 };
 
 }  // namespace
@@ -261,6 +263,8 @@ struct numpmp_gpu {
   // peer-memory exchange (pmp_p2p.cuh); xregion = [v | slots | xs | flags],
   // cudaMalloc'd so that it can be exported with CUDA IPC
   bool p2p = false;
+  bool p2p_fused = false;  // one GPU per rank: wait + finalize inside the owner epilogue
+  bool p2p_cta_sysfence = std::getenv("NUMPMP_P2P_SYSFENCE") != nullptr;  // A/B: per-CTA system fences
   void* xregion = nullptr;
   size_t xregion_bytes = 0;
   int64_t mo = 0, l0 = 0, l1 = 0;
@@ -268,7 +272,6 @@ struct numpmp_gpu {
   void** peer_tables = nullptr;      // device: 4 tables of world pointers
   unsigned long long* done_cnt = nullptr;
   double* ep_part = nullptr;
-  double* k1_scalars = nullptr;
   int64_t dev_bytes = 0;
   bool l2_guard_held = false;  // holds a reference on the device's persisting-L2 limit
   // get_state fingerprint: set_state of exactly the state the handle last
@@ -334,7 +337,7 @@ struct numpmp_gpu {
   int nb() const { return static_cast<int>(blocks.size()); }
   // kernel launches of one iteration (the NCCL all-reduce is not ours)
   int launches_per_iteration() const {
-    return p2p ? 2 * nb() + 3 : 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
+    return p2p ? 2 * nb() + (p2p_fused ? 1 : 3) : 2 * nb() + ((sharded || split_epilogue) ? 1 : 0);
   }
   std::vector<int> launch_side;  // per launch of an iteration: 1 stream side, 2 link side
 };
@@ -385,7 +388,7 @@ P2PArgs p2p_args(const numpmp_gpu* h) {
   p.flags = reinterpret_cast<unsigned long long*>(static_cast<char*>(h->xregion) + xr_flags_off(h));
   p.done_cnt = h->done_cnt;
   p.ep_part = h->ep_part;
-  p.k1_scalars = h->k1_scalars;
+  p.cta_sysfence = h->p2p_cta_sysfence ? 1 : 0;
   return p;
 }
 
@@ -454,6 +457,8 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.first = b == 0;
   k.row_mode = cb.row_mode;
   k.pair_tiles = cb.pair_tiles;
+  k.ix = cb.ix;
+  k.ix_off = cb.ix_off;
   k.row_ptr = cb.row_ptr;
   k.m = h->m;
   k.pieces = cb.pieces;
@@ -516,7 +521,9 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    if (bk.pair_tiles == 4)
+    if (bk.ix)
+      k_stream_pass_ix<<<h->grid1, kThreads, 0, s1>>>(a, bk);
+    else if (bk.pair_tiles == 4)
       k_stream_pass<4><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else if (bk.pair_tiles == 2)
       k_stream_pass<2><<<h->grid1, kThreads, 0, s1>>>(a, bk);
@@ -538,10 +545,13 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     mark(2);
     if (pipelined) CK(cudaEventRecord(ev_k2[b], h->stream));
   }
-  if (h->p2p) {
+  if (h->p2p && h->p2p_fused) {
+    k_p2p_epilogue<true><<<h->grid3, kThreads, 0, h->stream>>>(a);
+    mark(2);
+  } else if (h->p2p) {
     k_p2p_wait<0><<<1, 32, 0, h->stream>>>(a);
     mark(2);
-    k_p2p_epilogue<<<h->grid3, kThreads, 0, h->stream>>>(a);
+    k_p2p_epilogue<false><<<h->grid3, kThreads, 0, h->stream>>>(a);
     mark(2);
     k_p2p_finalize<<<1, 32, 0, h->stream>>>(a);
     mark(2);
@@ -757,6 +767,41 @@ int choose_blocks(int64_t n) {
 // segment bound is kSeg, raised so that the longest row fits one warp unit
 // (32 segments); consecutive whole rows are then packed greedily into units
 // of <= 32 segments (host pass over the per-row segment counts).
+// Interleaved route tiles of one column block (k_ix_tile_rows / k_ix_fill,
+// pmp_aux.cuh): rows per tile = its longest route, exclusive scan -> ix_off.
+void build_interleaved(numpmp_gpu* h, ColBlock& cb, int64_t* bytes) {
+  const long long ntiles = (cb.s1 - cb.s0 + 31) / 32;
+  if (ntiles == 0) return;
+  double max_pad = 2.0;
+  if (const char* env = std::getenv("NUMPMP_IX_MAX_PAD")) max_pad = std::atof(env);
+  int64_t tmpb = 0;
+  unsigned* off = dalloc<unsigned>(static_cast<size_t>(ntiles) + 1, &tmpb, h->stream);
+  unsigned* rows = dalloc<unsigned>(static_cast<size_t>(ntiles) + 1, &tmpb, h->stream);
+  CK(cudaMemsetAsync(rows + ntiles, 0, sizeof(unsigned), h->stream));
+  k_ix_tile_rows<<<grid_for(ntiles * 32), 256, 0, h->stream>>>(h->col_ptr, cb.s0, cb.s1, rows);
+  CK(cudaGetLastError());
+  size_t temp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, rows, off, static_cast<int>(ntiles + 1), h->stream));
+  void* temp = nullptr;
+  CK(lib_malloc_async(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
+  CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, rows, off, static_cast<int>(ntiles + 1), h->stream));
+  unsigned total = 0;
+  CK(cudaMemcpyAsync(&total, off + ntiles, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFreeAsync(temp, h->stream);
+  cudaFreeAsync(rows, h->stream);
+  if (static_cast<double>(total) * 32.0 > max_pad * static_cast<double>(std::max<int64_t>(cb.nnz, 1))) {
+    cudaFreeAsync(off, h->stream);  // skewed route lengths: the staged form
+    return;
+  }
+  // the offsets move from the temporary count into the handle's accounting
+  cb.ix_off = off;
+  *bytes += static_cast<int64_t>(sizeof(unsigned)) * (ntiles + 1);
+  cb.ix = dalloc<int>(static_cast<size_t>(total) * 32 + kIdxPad, bytes, h->stream);
+  k_ix_fill<<<grid_for(ntiles * 32), 256, 0, h->stream>>>(h->col_ptr, h->row_idx, cb.s0, cb.s1, cb.ix_off, cb.ix);
+  CK(cudaGetLastError());
+}
+
 void segment_block(numpmp_gpu* h, ColBlock& cb) {
   const int64_t m = h->m;
   int64_t tmpb = 0;
@@ -887,10 +932,11 @@ void preload_kernels(int device) {
   if (device < 0 || device >= 64 || done[device]) return;
   std::vector<const void*> f;
 #define NUMPMP_K(k) f.push_back(reinterpret_cast<const void*>(&k))
-  NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>);
+  NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>); NUMPMP_K(k_stream_pass_ix);
+  NUMPMP_K(k_ix_tile_rows); NUMPMP_K(k_ix_fill);
   NUMPMP_K(k_link_epilogue<0>); NUMPMP_K(k_link_epilogue<1>);
   NUMPMP_K(k_refresh_v); NUMPMP_K(k_set_v); NUMPMP_K(k_residual_parts);
-  NUMPMP_K(k_p2p_wait<0>); NUMPMP_K(k_p2p_epilogue); NUMPMP_K(k_p2p_finalize);
+  NUMPMP_K(k_p2p_wait<0>); NUMPMP_K(k_p2p_epilogue<false>); NUMPMP_K(k_p2p_epilogue<true>); NUMPMP_K(k_p2p_finalize);
   NUMPMP_K(k_p2p_aux_wait); NUMPMP_K(k_p2p_aux_signal); NUMPMP_K(k_p2p_push_partials);
   NUMPMP_K(k_p2p_reduce_bcast); NUMPMP_K(k_p2p_push_owned); NUMPMP_K(k_p2p_push_scalars);
   NUMPMP_K(k_p2p_sum_scalars);
@@ -1011,6 +1057,14 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
 
   // Column blocks (stream ranges rounded to 32-stream tiles) and their CSRs.
   const int nbk = choose_blocks(n);
+  // NUMPMP_K1_IX=1: K1 on interleaved route tiles where the padding to each
+  // tile's longest route costs at most NUMPMP_IX_MAX_PAD x the block's
+  // nonzeros (default 2; C: 1.68).  Off by default: one 128-byte index load
+  // per gather row instead of one 512-byte load per 128 entries is +4.5% L1->L2
+  // requests, and the passes are request-bound: C K1 0.468 -> 0.490 ms, B
+  // -1.4% (profiles/r2_k1_interleaved_ab.txt)
+  bool k1_ix = false;
+  if (const char* env = std::getenv("NUMPMP_K1_IX")) k1_ix = std::atoi(env) != 0;
   CK(cudaMemsetAsync(h->deg, 0, sizeof(int) * static_cast<size_t>(m), h->stream));
   for (int k = 0; k < nbk; ++k) {
     ColBlock cb;
@@ -1034,6 +1088,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
     CK(cudaGetLastError());
     segment_block(h, h->blocks.back());
+    if (h->blocks.back().pair_tiles == 1 && k1_ix) build_interleaved(h, h->blocks.back(), b);
   }
   CK(cudaStreamSynchronize(h->stream));
   pt.mark("create: device CSR build");
@@ -1043,6 +1098,11 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
+  for (const ColBlock& cb : h->blocks)
+    if (cb.ix) {  // the interleaved stream pass: its own occupancy
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass_ix, kThreads, 0));
+      break;
+    }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 2>, kThreads, 0));
   int occ3 = 0, occ2r = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
@@ -1241,6 +1301,24 @@ void p2p_wire(numpmp_gpu* h, const std::vector<void*>& bases) {
                      h->stream));
   CK(cudaStreamSynchronize(h->stream));
   h->p2p = true;
+  // One GPU per rank (no peer region on this device): the wait and the
+  // finalize fold into the owner epilogue (pmp_p2p.cuh, fused mode).  Ranks
+  // that share a GPU keep the separate one-CTA kernels, so a spinning CTA
+  // never holds SMs another rank's link pass needs.
+  bool distinct = true;
+  for (size_t q = 0; q < W; ++q) {
+    if (static_cast<int>(q) == h->rank) continue;
+    cudaPointerAttributes at{};
+    CK(cudaPointerGetAttributes(&at, bases[q]));
+    if (at.device == h->device) distinct = false;
+  }
+  h->p2p_fused = distinct;
+  // A/B: 0 off, 1 on where no rank shares this GPU; 2 on regardless (tests
+  // with grids small enough that spinning CTAs cannot starve a peer's kernels)
+  if (const char* env = std::getenv("NUMPMP_P2P_FUSED")) {
+    const int f = std::atoi(env);
+    h->p2p_fused = f == 2 || (f == 1 && distinct);
+  }
   for (int i = 0; i < 2; ++i) {  // captured graphs hold the old launch list
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
     h->graph[i] = nullptr;
@@ -1332,7 +1410,6 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
       h->done_cnt = dalloc<unsigned long long>(4, b, h->stream);
       CK(cudaMemsetAsync(h->done_cnt, 0, 4 * sizeof(unsigned long long), h->stream));
       h->ep_part = dalloc<double>(4 * static_cast<size_t>(h->grid3), b, h->stream);
-      h->k1_scalars = dalloc<double>(2, b, h->stream);
       h->peer_tables = dalloc<void*>(4 * static_cast<size_t>(world), b, h->stream);
       CK(cudaStreamSynchronize(h->stream));
     } else if (h->sharded) {
@@ -2074,7 +2151,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
   }
   std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
-                             h->done_cnt, h->ep_part, h->k1_scalars, h->peer_tables,
+                             h->done_cnt, h->ep_part, h->peer_tables,
                              h->v_alt[0], h->v_alt[1],
                              h->Lbuf,    h->Lacc,    h->k1_part,   h->k2_part,    h->scratch_m,
                              h->scratch_m2, h->scratch_n, h->scalars, h->ctrl, h->trace_dev};
@@ -2096,7 +2173,8 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
                     static_cast<void*>(cb.units), static_cast<void*>(cb.vptr),
                     static_cast<void*>(cb.vrow), static_cast<void*>(cb.pieces),
-                    static_cast<void*>(cb.uctr), static_cast<void*>(cb.upart)})
+                    static_cast<void*>(cb.uctr), static_cast<void*>(cb.upart),
+                    static_cast<void*>(cb.ix), static_cast<void*>(cb.ix_off)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {

@@ -12,7 +12,13 @@ Cases:
   B      config B (1M streams / 100k links), 20 iterations
   p2p1   the peer-memory engine, world 1 (fused owner epilogue)
   p2p2   world 2 in this process on one GPU (separate wait / finalize
-         kernels): the system-scope barriers and the slot / v / xs exchange
+         kernels).  The sanitizers serialize a process's kernels, so the
+         ranks' barrier spin cannot complete here (it traps after 60 s);
+         use ipcrank instead.
+  ipcrank R PORT  rank R of 2 over CUDA IPC (one process per rank, both on
+         cuda:0, gloo for the 64-byte handles): run two of these, each under
+         its own compute-sanitizer, for the exchange's barriers and the
+         slot / v / xs stores between processes
 """
 import os
 import sys
@@ -101,9 +107,38 @@ def p2p_case(world):
     return ok
 
 
+def ipc_rank(rank, port):
+    import torch.distributed as dist
+
+    from paper_2509_10722_b200.shard import ShardedPmpSolver
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    p = gen(1200, 2500, 5.0, 2, True, 3)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0, max_iters=200)
+
+    def allgather(mine):
+        out = [None, None]
+        dist.all_gather_object(out, mine)
+        return out
+
+    s = ShardedPmpSolver(p, cfg, rank, 2, device=0, exchange="p2p", ipc_allgather=allgather)
+    sol = s.solve()
+    s.close()
+    dist.destroy_process_group()
+    ref = R.solve(o.arrays_from(p), ocfg(cfg))
+    ok = sol.iterations == ref.iterations
+    print(f"ipc rank {rank}/2: iterations {sol.iterations} (oracle {ref.iterations}) {'ok' if ok else 'MISMATCH'}",
+          flush=True)
+    return ok
+
+
 CASES = {"A": case_A, "forms": case_forms, "B": case_B, "p2p1": lambda: p2p_case(1), "p2p2": lambda: p2p_case(2)}
 
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["ipcrank"]:
+        sys.exit(0 if ipc_rank(int(sys.argv[2]), int(sys.argv[3])) else 1)
     names = sys.argv[1:] or list(CASES)
     good = all([CASES[n]() for n in names])
     sys.exit(0 if good else 1)

@@ -324,6 +324,49 @@ def test_p2p_exchange_ranks_match_oracle(world, blocks, restatement, oracle_mod,
     assert link_owners(p.m, world)[-1] == p.m
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_p2p_fused_epilogue_matches_oracle(world, restatement, oracle_mod, monkeypatch):
+    # Fused mode (one GPU per rank in production: the "loads stored" wait in
+    # every owner-epilogue CTA, the finalize in its last CTA, 2 NB + 1
+    # launches per iteration).  Forced here with ranks sharing one GPU; the
+    # grids of this small instance leave SMs free for every rank's kernels.
+    import ctypes as C
+
+    from paper_2509_10722_b200 import _lib
+    from paper_2509_10722_b200.shard import p2p_local_group, run_ranks
+
+    monkeypatch.setenv("NUMPMP_P2P_FUSED", "2")
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", "2")
+    p = _gen(1500, 3000, 6.0, 2, True, 23)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    ranks = p2p_local_group(p, cfg, world)
+    L = _lib.lib()
+    try:
+        for s in ranks:
+            assert L.numpmp_gpu_set_profiling(s.handle(), 1) == 0
+        sols = run_ranks([s.solve for s in ranks])
+        launches, iters = C.c_int64(), C.c_int64()
+        k1, k2 = C.c_double(), C.c_double()
+        assert L.numpmp_gpu_profile(ranks[0].handle(), C.byref(launches), C.byref(k1), C.byref(k2),
+                                    C.byref(iters)) == 0
+    finally:
+        for s in ranks:
+            s.close()
+    # launches are counted per queued 32-iteration batch: 2 NB + 1 = 5 per
+    # iteration fused (7 with the separate wait and finalize kernels)
+    batches = -(-iters.value // 32)
+    assert iters.value > 0 and launches.value % (32 * 5) == 0
+    assert batches <= launches.value // (32 * 5) <= batches + 2
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    x = np.concatenate([s.x for s in sols])
+    for s in sols:
+        assert s.iterations == ref.iterations
+        np.testing.assert_array_equal(s.lambda_raw, sols[0].lambda_raw)
+    for got, want in [(x, ref.x), (sols[0].lambda_raw, ref.lambda_raw), (sols[0].s, ref.s)]:
+        ok, err = close(got, want)
+        assert ok, err
+
+
 def test_p2p_exchange_repeated_and_warm_solves(restatement, oracle_mod):
     # the same ranks solving again (cold) and warm-started: each start state
     # must rebuild v on every rank, whatever the previous solve left there
@@ -917,6 +960,32 @@ def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restate
     for got, want in [(sol.x, ref.x), (sol.lambda_raw, ref.lambda_raw), (sol.s, ref.s)]:
         ok, err = close(got, want)
         assert ok, err
+
+
+@pytest.mark.parametrize("blocks", ["1", "3"])
+def test_interleaved_stream_pass_is_bit_identical_to_staged(blocks, restatement, oracle_mod, monkeypatch):
+    # k_stream_pass_ix (interleaved route tiles, BlockArgs::ix) sums every
+    # route in route order like the staged form: the whole solve must be
+    # bit-identical.  Ragged tail (n % 32 != 0), routes of 1..~25 links,
+    # 1 and 3 column blocks; NUMPMP_IX_MAX_PAD=1 forces the staged form.
+    monkeypatch.setenv("NUMPMP_COL_BLOCKS", blocks)
+    monkeypatch.setenv("NUMPMP_K1_IX", "1")
+    p = _gen(3000, 7001, 10.0, 2, True, 17)
+    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
+    sols = {}
+    for mode in ("ix", "staged"):
+        monkeypatch.setenv("NUMPMP_IX_MAX_PAD", "2" if mode == "ix" else "1")
+        with pmp.PmpSolver(p, cfg) as s:
+            sols[mode] = s.solve()
+    a, b = sols["ix"], sols["staged"]
+    assert a.iterations == b.iterations
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
+    assert a.objective == b.objective and a.r_norm == b.r_norm and a.s_norm == b.s_norm
+    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
+    assert a.iterations == ref.iterations
+    ok, err = close(a.x, ref.x)
+    assert ok, err
 
 
 @pytest.mark.parametrize("pair_tau,tile_q", [("0", "2"), ("100", "2"), ("100", "4")])
