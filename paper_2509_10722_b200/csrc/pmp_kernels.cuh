@@ -944,6 +944,20 @@ __device__ __forceinline__ T* ld_ptr(T* const* p) {
 __device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
   asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
 }
+// Signal every rank's counter `which` with ONE system-scope release: a
+// fence.acq_rel.sys followed by relaxed reductions is a release pattern for
+// each of them (cumulative over everything this thread has observed,
+// including the other CTAs' stores ordered before their tickets).  A
+// red.release.sys per peer would put `world` system fences, and a
+// fence.sc.sys (__threadfence_system) a stronger one, on the critical path
+// of the barrier (profiles/r2_p2p_fences.txt).
+__device__ __forceinline__ void signal_all_sys(unsigned long long* const* flags_peer, int world, int which) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int q = 0; q < world; ++q) {
+    unsigned long long* c = ld_ptr(flags_peer + q) + which;
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(c) : "memory");
+  }
+}
 
 // Link-pass gather over one column block's CSR, in "warp units": the rows
 // (links) are cut into segments of <= seg entries (near-equal split; every
@@ -1083,8 +1097,7 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
     if (!s_last || threadIdx.x != 0) return;
     // (the stream-pass scalars are summed by the owner epilogue's last CTA)
     a.ctrl->ticket2 = 0;
-    __threadfence_system();
-    for (int q = 0; q < a.p2p.world; ++q) signal_sys(a.p2p.flags_peer[q] + 0);  // "loads stored"
+    signal_all_sys(a.p2p.flags_peer, a.p2p.world, 0);  // "loads stored"
     return;
   }
   if (kPhase == LP_GATHER) {

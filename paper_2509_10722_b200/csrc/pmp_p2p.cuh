@@ -81,8 +81,7 @@ __device__ __forceinline__ void p2p_wait_counter(const P2PArgs& p, int which) {
 }
 
 __device__ __forceinline__ void p2p_signal_all(const P2PArgs& p, int which) {
-  __threadfence_system();
-  for (int q = 0; q < p.world; ++q) signal_sys(ld_ptr(p.flags_peer + q) + which);
+  signal_all_sys(p.flags_peer, p.world, which);
 }
 
 // ---------------------------------------------------------------- iteration
