@@ -940,10 +940,6 @@ __device__ __forceinline__ T* ld_ptr(T* const* p) {
   return reinterpret_cast<T*>(__ldg(reinterpret_cast<const unsigned long long*>(p)));
 }
 
-// System-scope release increment of a (possibly peer) barrier counter.
-__device__ __forceinline__ void signal_sys(unsigned long long* ctr) {
-  asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
-}
 // Signal every rank's counter `which` with ONE system-scope release: a
 // fence.acq_rel.sys followed by relaxed reductions is a release pattern for
 // each of them (cumulative over everything this thread has observed,
@@ -1082,8 +1078,8 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
     // The CTA's peer stores, then a fence before the ticket (the grid.sync
     // pattern: bar.sync orders the CTA's writes before thread 0's cumulative
     // fence).  The ticket is observed on this GPU only, so a gpu-scope fence
-    // orders the stores before it; the last CTA's system-scope fence +
-    // red.release.sys is cumulative over everything it observed, which makes
+    // orders the stores before it; the last CTA's system-scope release
+    // (signal_all_sys) is cumulative over everything it observed, which makes
     // every CTA's peer stores visible to the peers that acquire the signal.
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -43,7 +43,7 @@
 // stored"(k), i.e. after every rank's stream passes of iteration k.
 //
 // Barrier counters are cumulative (flags[i] on the receiving rank, bumped by
-// every rank with red.release.sys); done_cnt[i] counts the barriers of kind
+// every rank with one fence.acq_rel.sys + red.relaxed.sys); done_cnt[i] counts the barriers of kind
 // i this rank has completed, identical on all ranks because every rank runs
 // the same sequence: target = world * (done_cnt[i] + 1).
 //   flags[0] loads stored / aux push, flags[1] epilogue done / aux result,
