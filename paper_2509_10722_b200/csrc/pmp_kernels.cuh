@@ -683,183 +683,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 
-// ------------------------------------------- K1, tile prologue prefetched
-// The stream pass's per-tile chain is offsets (col_ptr, HBM) -> span ->
-// index round (HBM) -> gathers; with 3-link routes (config E) the two HBM
-// round trips, not the gathers, set the pace (ncu: the top stalls are the
-// shuffle on the offsets and the shared-memory store of the indices,
-// profiles/r2_ncu_E_summary.csv).  Here both are issued ahead with cp.async
-// into per-warp shared buffers, no registers held: the offsets two tiles
-// ahead, the first index round one tile ahead.  A tile then finds its
-// offsets and first round in shared memory; rounds beyond the first (spans
-// > kStageInts) are loaded as in warp_segments_sum_q.  Same gathers, same
-// order, same sums: bit-identical to k_stream_pass<Q>.
-__device__ __forceinline__ void cp_async4(int* smem, const int* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16(int* smem, const int* gmem, uint64_t pol) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-constexpr int kOffStride = 132;  // >= 32 * 4 + 1 offsets per tile buffer
-template <int Q>
-__device__ __forceinline__ void pf_offsets(const int* __restrict__ col_ptr, long long j0, long long s1, int* soff,
-                                           int lane) {
-  for (int k = lane; k <= 32 * Q; k += 32) cp_async4(soff + k, col_ptr + min(j0 + k, s1));
-}
-__device__ __forceinline__ void pf_round(const int* __restrict__ idx, const int* soff_last, int span_beg, int* sidx,
-                                         int lane, uint64_t pol) {
-  const int span_end = *soff_last;
-  const int cb = span_beg & ~3;
-#pragma unroll
-  for (int i = 0; i < kStageInts / 128; ++i) {
-    const int o = 4 * (lane + 32 * i);
-    if (cb + o < span_end) cp_async16(sidx + o, idx + cb + o, pol);
-  }
-}
-
-template <int Q, class G>
-__device__ __forceinline__ void stream_pass_pf(const IterArgs& a, const BlockArgs& bk, G g, double rho,
-                                               bool trace_it, int* soff_w /* 3 x kOffStride */,
-                                               int* sidx_w /* 2 x kStageInts */, double& p_tda2,
-                                               double& p_obj) {
-  constexpr int NV = kStageInts / 128;
-  constexpr int H = kUnroll / Q;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_last = policy_evict_last();
-  const long long ngroups = (bk.s1 - bk.s0 + 32 * Q - 1) / (32 * Q);
-  const long long S = (long long)gridDim.x * kWarps;
-  long long pt = (long long)blockIdx.x * kWarps + wib;
-  int ob = 0, ib = 0;
-  // prologue: offsets of the first two tiles, the first tile's first round
-  if (pt < ngroups) pf_offsets<Q>(a.col_ptr, bk.s0 + pt * 32 * Q, bk.s1, soff_w, lane);
-  cp_async_commit();
-  if (pt + S < ngroups) pf_offsets<Q>(a.col_ptr, bk.s0 + (pt + S) * 32 * Q, bk.s1, soff_w + kOffStride, lane);
-  cp_async_commit();
-  cp_async_wait<1>();
-  __syncwarp();
-  if (pt < ngroups) pf_round(a.row_idx, soff_w + 32 * Q, soff_w[0], sidx_w, lane, pol_first);
-  cp_async_commit();
-  for (; pt < ngroups; pt += S) {
-    int* so = soff_w + ob * kOffStride;
-    int* si = sidx_w + ib * kStageInts;
-    if (pt + 2 * S < ngroups)
-      pf_offsets<Q>(a.col_ptr, bk.s0 + (pt + 2 * S) * 32 * Q, bk.s1, soff_w + ((ob + 2) % 3) * kOffStride, lane);
-    cp_async_commit();
-    // independent of the offsets: issued before the wait
-    const long long base = bk.s0 + pt * 32 * Q + lane;
-    int kd[Q];
-    double A[Q], w[Q], sum[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const long long j = base + 32 * q;
-      A[q] = 0.0;
-      w[q] = 0.0;
-      kd[q] = 0;
-      if (j < bk.s1) {
-        A[q] = ld_stream_f64(a.A_in + j, pol_first);
-        w[q] = __ldg(a.w + j);
-        kd[q] = __ldg(a.kind + j);
-      }
-    }
-    cp_async_wait<1>();  // all but the newest group: this tile's round, the next tile's offsets
-    __syncwarp();
-    if (pt + S < ngroups) {
-      const int* sn = soff_w + ((ob + 1) % 3) * kOffStride;
-      pf_round(a.row_idx, sn + 32 * Q, sn[0], sidx_w + (ib ^ 1) * kStageInts, lane, pol_first);
-    }
-    cp_async_commit();
-    int b[Q], e[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      b[q] = so[32 * q + lane];
-      e[q] = so[32 * q + lane + 1];
-      sum[q] = 0.0;
-    }
-    const int span_beg = so[0], span_end = so[32 * Q];
-    int cb = span_beg & ~3;
-    bool first = true;
-    while (cb < span_end) {
-      const int c1 = min(cb + kStageInts, span_end);
-      if (!first) {  // rounds beyond the prefetched one (long spans)
-        int4 buf[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const int gp = cb + 4 * (lane + 32 * i);
-          if (gp < c1) buf[i] = ld_stream_int4(a.row_idx + gp, pol_first);
-        }
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const int o = 4 * (lane + 32 * i);
-          if (cb + o < c1) *reinterpret_cast<int4*>(si + o) = buf[i];
-        }
-        __syncwarp();
-      }
-      first = false;
-      int k[Q], hi[Q];
-      bool more = false;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        k[q] = max(b[q], cb);
-        hi[q] = min(e[q], c1);
-        more = more || k[q] < hi[q];
-      }
-      while (more) {
-        double vv[Q][H];
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-#pragma unroll
-          for (int u = 0; u < H; ++u) vv[q][u] = (k[q] + u < hi[q]) ? g(si[k[q] + u - cb]) : 0.0;
-        more = false;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-#pragma unroll
-          for (int u = 0; u < H; ++u)
-            if (k[q] + u < hi[q]) sum[q] += vv[q][u];
-          k[q] += H;
-          more = more || k[q] < hi[q];
-        }
-      }
-      __syncwarp();
-      cb += kStageInts;
-    }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      asm volatile("" : "+r"(kd[q]), "+d"(w[q]) : : "memory");
-      const long long j = base + 32 * q;
-      if (j < bk.s1)
-        stream_update(a, j, b[q], e[q], A[q], w[q], kd[q], sum[q], rho, trace_it, p_tda2, p_obj, pol_first,
-                      pol_last);
-    }
-    ob = (ob + 1) % 3;
-    ib ^= 1;
-  }
-  cp_async_wait<0>();
-}
-
-template <int kQ>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass_pf(IterArgs a, BlockArgs bk) {
-  __shared__ __align__(16) int sidx[kWarps][2 * kStageInts];
-  __shared__ __align__(16) int soff[kWarps][3 * kOffStride];
-  if (kernel_should_exit(a.ctrl)) return;
-  const double rho = a.ctrl->rho;
-  const long long k = a.ctrl->run_k + 1;
-  const bool trace_it = (a.mode == MODE_RUN) && (k % a.trace_every == 0);
-  double part[2] = {0.0, 0.0};
-  const int sel = a.ctrl->v_sel;
-  const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  const int wib = threadIdx.x >> 5;
-  stream_pass_pf<kQ>(a, bk, GatherV{v}, rho, trace_it, soff[wib], sidx[wib], part[0], part[1]);
-  block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
-}
-
 // Interleaved route tiles (BlockArgs::ix): a warp's 32 streams read their
 // routes row by row, one coalesced 128-byte index load per row feeding one
 // gather per lane, the next batch's index rows in flight while the current

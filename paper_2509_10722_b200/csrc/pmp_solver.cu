@@ -253,7 +253,6 @@ struct numpmp_gpu {
   cudaEvent_t pipe_ev[2 * kMaxBlocks + 2] = {};
   bool split_epilogue = true;      // NUMPMP_SPLIT_EPILOGUE=0: epilogue fused into the last link pass
   bool pipeline = true;            // NUMPMP_PIPELINE=0: serial graph (K1(b+1) no longer overlaps K2(b))
-  bool k1_pf = false;              // NUMPMP_K1_PF=1: stream pass with the tile prologue prefetched (cp.async)
   std::string err;
   numpmp_config cfg{};
   int64_t m = 0, n = 0, nnz = 0;
@@ -524,10 +523,6 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
     if (bk.ix)
       k_stream_pass_ix<<<h->grid1, kThreads, 0, s1>>>(a, bk);
-    else if (h->k1_pf && bk.pair_tiles == 1)
-      k_stream_pass_pf<1><<<h->grid1, kThreads, 0, s1>>>(a, bk);
-    else if (h->k1_pf && bk.pair_tiles == 2)
-      k_stream_pass_pf<2><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else if (bk.pair_tiles == 4)
       k_stream_pass<4><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else if (bk.pair_tiles == 2)
@@ -938,7 +933,6 @@ void preload_kernels(int device) {
   std::vector<const void*> f;
 #define NUMPMP_K(k) f.push_back(reinterpret_cast<const void*>(&k))
   NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>); NUMPMP_K(k_stream_pass_ix);
-  NUMPMP_K(k_stream_pass_pf<1>); NUMPMP_K(k_stream_pass_pf<2>);
   NUMPMP_K(k_ix_tile_rows); NUMPMP_K(k_ix_fill);
   NUMPMP_K(k_link_epilogue<0>); NUMPMP_K(k_link_epilogue<1>);
   NUMPMP_K(k_refresh_v); NUMPMP_K(k_set_v); NUMPMP_K(k_residual_parts);
@@ -975,7 +969,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   for (cudaEvent_t& e : h->pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* env = std::getenv("NUMPMP_SPLIT_EPILOGUE")) h->split_epilogue = std::atoi(env) != 0;
   if (const char* env = std::getenv("NUMPMP_PIPELINE")) h->pipeline = std::atoi(env) != 0;
-  if (const char* env = std::getenv("NUMPMP_K1_PF")) h->k1_pf = std::atoi(env) != 0;
   // L2 set-aside for the evict_last lines (x of the live column blocks, v):
   // 32 MB measured best at config C (profiles/r1_l2_sweep.txt);
   // NUMPMP_L2_PERSIST_MB overrides (0 = leave the device limit alone).
@@ -1105,11 +1098,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
-  if (h->k1_pf) {  // the prefetching stream pass: its own occupancy (shared-memory buffers)
-    int occ_pf = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_pf, k_stream_pass_pf<1>, kThreads, 0));
-    occ1 = std::min(occ1, occ_pf);
-  }
   for (const ColBlock& cb : h->blocks)
     if (cb.ix) {  // the interleaved stream pass: its own occupancy
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass_ix, kThreads, 0));
