@@ -64,6 +64,14 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
 constexpr int kStageInts = NUMPMP_STAGE_INTS;  // staged indices per warp and round
 constexpr int kUnroll = NUMPMP_GATHER_UNROLL;  // gathers in flight per lane
+// Multi-route stream tiles (short routes, 64-128 streams per warp: spans of
+// ~200 indices at config E) stage rounds of 256: half the shared memory,
+// more L1 for the gathered v, which consecutive transit tiles reuse
+// (E: K1 -5.5%, profiles/r2_stage_ints_ab.txt)
+#ifndef NUMPMP_STAGE_Q
+#define NUMPMP_STAGE_Q 256
+#endif
+constexpr int kStageQ = NUMPMP_STAGE_Q;
 constexpr int kSeg = kStageInts / 32;          // target entries per link segment (one staged round per warp)
 constexpr int kSplitMin = 32 * kSeg;           // rows longer than this are split into pieces
 #ifndef NUMPMP_PIECE_ROUNDS
@@ -421,12 +429,12 @@ __device__ __forceinline__ double warp_strided_sum(const int* __restrict__ idx, 
 // within each q, segment q+1 after segment q across the warp): each batch
 // issues kUnroll/Q gathers from every segment, so a lane with Q short routes
 // keeps all of them in flight at once.  Each segment is summed in index order.
-template <int Q, class G>
+template <int Q, int kStage, class G>
 __device__ __forceinline__ void warp_segments_sum_q(const int* __restrict__ idx, int span_beg,
                                                     int span_end, const int (&b)[Q], const int (&e)[Q],
                                                     int* __restrict__ sidx, int lane, G g,
                                                     uint64_t pol_stream, double (&acc)[Q]) {
-  constexpr int NV = kStageInts / 128;
+  constexpr int NV = kStage / 128;
   constexpr int H = kUnroll / Q;
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = 0.0;
@@ -438,14 +446,14 @@ __device__ __forceinline__ void warp_segments_sum_q(const int* __restrict__ idx,
     if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
   }
   while (cb < span_end) {
-    const int c1 = min(cb + kStageInts, span_end);
+    const int c1 = min(cb + kStage, span_end);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int o = 4 * (lane + 32 * i);
       if (cb + o < c1) *reinterpret_cast<int4*>(sidx + o) = buf[i];
     }
     __syncwarp();
-    const int nb = cb + kStageInts;
+    const int nb = cb + kStage;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int gp = nb + 4 * (lane + 32 * i);
@@ -651,7 +659,7 @@ __device__ __forceinline__ void stream_pass_multi(const IterArgs& a, const Block
     int span_end = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) span_end = max(span_end, __shfl_sync(kFull, end[q], 31));
-    warp_segments_sum_q<Q>(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g, pol_first, sum);
+    warp_segments_sum_q<Q, kStageQ>(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g, pol_first, sum);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       asm volatile("" : "+r"(kd[q]), "+d"(w[q]) : : "memory");
@@ -667,7 +675,7 @@ __device__ __forceinline__ void stream_pass_multi(const IterArgs& a, const Block
 // short routes) -- separate instantiations, each with its own registers.
 template <int kQ>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts];
+  __shared__ __align__(16) int sidx[kWarps][kQ > 1 ? kStageQ : kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;
   const long long k = a.ctrl->run_k + 1;
