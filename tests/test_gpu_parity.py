@@ -686,11 +686,14 @@ def test_config_f_full_solve_properties():
     assert np.min(sol.lambda_) >= 0.0
 
 
-def _ipc_rank(rank, world, port, q):
+def _ipc_rank(rank, world, port, q, fused=None):
     # one process per rank, all on cuda:0 (the box has one GPU): the real
     # CUDA IPC path of the exchange (export -> all_gather -> open), gloo for
     # the 64-byte handles
     import os
+
+    if fused is not None:
+        os.environ["NUMPMP_P2P_FUSED"] = fused
 
     import torch.distributed as dist
 
@@ -715,7 +718,12 @@ def _ipc_rank(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_p2p_exchange_over_cuda_ipc_processes(restatement, oracle_mod):
+@pytest.mark.parametrize("fused", [None, "2"])
+def test_p2p_exchange_over_cuda_ipc_processes(fused, restatement, oracle_mod):
+    # fused "2": the one-GPU-per-rank owner epilogue (wait and finalize inside
+    # it) forced across the two processes; they time-slice the GPU, so a
+    # spinning epilogue only delays the other rank's kernels, and the
+    # cross-process acquire / release protocol of the production path runs
     import socket
 
     import torch.multiprocessing as tmp
@@ -727,7 +735,7 @@ def test_p2p_exchange_over_cuda_ipc_processes(restatement, oracle_mod):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     world = 2
-    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, q, fused)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
