@@ -434,10 +434,10 @@ def run_ours(args):
     iter_ms = (ms1.value + ms2.value) / n_it
     iter_gbs = (k1b + k2b) / (iter_ms * 1e-3) / 1e9
     # DRAM traffic of the dominant kernel per iteration, from the committed
-    # ncu --set full capture (profiles/traffic_r1.json; config C, one GPU)
+    # ncu --set full capture (profiles/traffic_r2.json; config C, one GPU)
     traffic, xbar_pct, iter_dram = None, None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic_r1.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic_r2.json")) as f:
             tr = json.load(f)
         if tr.get("config") == name and world == 1:
             key = "k_link_pass" if avg2 >= avg1 else "k_stream_pass"
@@ -564,7 +564,7 @@ def run_ours(args):
                                           "frac": gather_rate / gather_peak,
                                           "l1_to_l2_request_pct_ncu": xbar_pct,
                                           "source": "scripts/gather_lanes_bench.cu (profiles/r1_gather_lanes.txt); "
-                                                    "request utilisation: profiles/traffic_r1.json"}},
+                                                    "request utilisation: profiles/traffic_r2.json"}},
             "iteration_roofline": {"alg_bytes": k1b + k2b, "alg_bytes_per_nnz": (k1b + k2b) / max(lp.nnz, 1),
                                    "dram_bytes_ncu": iter_dram,
                                    "dram_bytes_per_nnz_ncu": (iter_dram / max(lp.nnz, 1)) if iter_dram else None,
