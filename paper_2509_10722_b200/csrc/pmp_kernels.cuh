@@ -379,43 +379,6 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
   return acc;
 }
 
-#ifndef NUMPMP_ROW_STAGE
-#define NUMPMP_ROW_STAGE 0  // 0: row mode stages like the other forms; N: rounds of N via cp.async
-#endif
-constexpr int kRowStage = NUMPMP_ROW_STAGE > 0 ? NUMPMP_ROW_STAGE : kStageInts;
-__device__ __forceinline__ void cp_async16(int* smem, const int* gmem, uint64_t pol) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "l"(pol)
-               : "memory");
-}
-// warp_segments_sum with rounds of kStage indices copied global -> shared by
-// cp.async (no registers held for a prefetch, so a round can cover a whole
-// row-mode group of 32 links: every lane gathers in the same round).
-template <int kStage, class G>
-__device__ __forceinline__ double warp_segments_sum_async(const int* __restrict__ idx, int span_beg,
-                                                          int span_end, int seg_beg, int seg_end,
-                                                          int* __restrict__ sidx, int lane, G g,
-                                                          uint64_t pol_stream) {
-  double acc = 0.0;
-  for (int cb = span_beg & ~3; cb < span_end; cb += kStage) {
-    const int c1 = min(cb + kStage, span_end);
-    for (int o = 4 * lane; cb + o < c1; o += 128) cp_async16(sidx + o, idx + cb + o, pol_stream);
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
-    const int lo = max(seg_beg, cb), hi = min(seg_end, c1);
-    for (int k = lo; k < hi; k += kUnroll) {
-      double vv[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + u < hi) ? g(sidx[k + u - cb]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (k + u < hi) acc += vv[u];
-    }
-    __syncwarp();
-  }
-  return acc;
-}
-
 // Warp-cooperative gather-sum of one contiguous index range (a split-row
 // piece): rounds of kStageInts indices staged as in warp_segments_sum; lane
 // k gathers entries k, k+32, ... of each round, so one load instruction
@@ -1046,7 +1009,7 @@ template <int kPhase, int kForm>
 __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinBlocks) k_link_pass(IterArgs a, BlockArgs bk,
                                                                    const double* __restrict__ src,
                                                                    double* __restrict__ out) {
-  __shared__ __align__(16) int sidx[kWarps][kForm == 0 ? kRowStage : kStageInts];
+  __shared__ __align__(16) int sidx[kWarps][kStageInts];
   __shared__ bool s_last;
   if (a.mode != MODE_AUX && kernel_should_exit(a.ctrl)) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1084,11 +1047,8 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
       if (!bk.first && valid) Lprev = __ldcg(a.Lacc + r);
       const int span_beg = __shfl_sync(kFull, rb, 0);
       const int span_end = __shfl_sync(kFull, re, 31);
-      const double s = NUMPMP_ROW_STAGE > 0
-                           ? warp_segments_sum_async<kRowStage>(bk.col_idx, span_beg, span_end, rb, re,
-                                                                sidx[wib], lane, GatherX{src}, pol_first)
-                           : warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
-                                               GatherX{src}, pol_first);
+      const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
+                                         GatherX{src}, pol_first);
       if (valid) row_done(r, bk.first ? s : Lprev + s);
     }
   } else {
