@@ -59,9 +59,6 @@ namespace numpmp_dev {
 #ifndef NUMPMP_FLAT_GATHER
 #define NUMPMP_FLAT_GATHER 0
 #endif
-#ifndef NUMPMP_Q_PF_OFFS
-#define NUMPMP_Q_PF_OFFS 0
-#endif
 constexpr int kWarps = NUMPMP_WARPS;  // warps per block (gather passes)
 constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
@@ -638,45 +635,17 @@ __device__ __forceinline__ void stream_pass_multi(const IterArgs& a, const Block
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
   const long long ngroups = (bk.s1 - bk.s0 + 32 * Q - 1) / (32 * Q);
-#if NUMPMP_Q_PF_OFFS
-  // the next tile's offsets one tile ahead (4 registers at Q = 2)
-  int nbeg[Q], nend[Q];
-  {
-    const long long pt0 = (long long)blockIdx.x * kWarps + wib;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const long long j = bk.s0 + pt0 * 32 * Q + lane + 32 * q;
-      const bool v = pt0 < ngroups && j < bk.s1;
-      nbeg[q] = __ldg(a.col_ptr + (v ? j : bk.s1));
-      nend[q] = __ldg(a.col_ptr + (v ? j + 1 : bk.s1));
-    }
-  }
-#endif
   for (long long pt = (long long)blockIdx.x * kWarps + wib; pt < ngroups;
        pt += (long long)gridDim.x * kWarps) {
     int beg[Q], end[Q], kd[Q];
     double A[Q], w[Q], sum[Q];
     const long long base = bk.s0 + pt * 32 * Q + lane;
-#if NUMPMP_Q_PF_OFFS
-    const long long ptn = pt + (long long)gridDim.x * kWarps;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      beg[q] = nbeg[q];
-      end[q] = nend[q];
-      const long long jn = bk.s0 + ptn * 32 * Q + lane + 32 * q;
-      const bool vn = ptn < ngroups && jn < bk.s1;
-      nbeg[q] = __ldg(a.col_ptr + (vn ? jn : bk.s1));
-      nend[q] = __ldg(a.col_ptr + (vn ? jn + 1 : bk.s1));
-    }
-#endif
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const long long j = base + 32 * q;
       const bool v = j < bk.s1;
-#if !NUMPMP_Q_PF_OFFS
       beg[q] = __ldg(a.col_ptr + (v ? j : bk.s1));
       end[q] = __ldg(a.col_ptr + (v ? j + 1 : bk.s1));
-#endif
       A[q] = 0.0;
       w[q] = 0.0;
       kd[q] = 0;
