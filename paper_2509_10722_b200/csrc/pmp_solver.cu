@@ -23,6 +23,8 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a profiler attached
+
 #include "numpmp_gpu.h"
 #include "numpmp_host.h"
 #include "pmp_aux.cuh"
@@ -210,6 +212,15 @@ int grid_for(long long work, int threads = 256) {
   if (b > 148 * 32) b = 148 * 32;
   return static_cast<int>(b);
 }
+
+// One NVTX range per C-ABI call (profiler ranges for
+// ncu / nsys timelines), named after the entry point.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // NUMPMP_TIMING=1: host wall time of the setup / run / teardown phases on
 // stderr (end-to-end accounting of the C-ABI calls).
@@ -1353,6 +1364,7 @@ static int create_impl(const numpmp_problem_view* pv, const numpmp_config* cfg, 
                        int rank, int world, const void* nccl_id, int64_t stream_begin,
                        int64_t n_total, numpmp_gpu** out, int exchange = -1) {
   if (!out) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "out is null");
+  NvtxRange nvtx_range_("numpmp_gpu_create");
   *out = nullptr;
   if (!cfg) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "config is null");
   if (const char* msg = validate_config(cfg)) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, msg);
@@ -1458,6 +1470,7 @@ int numpmp_gpu_create_sharded(const numpmp_problem_view* shard, const numpmp_con
 #define GUARD(h, ...)                                                   \
   do {                                                                  \
     if (!(h)) return set_err(nullptr, NUMPMP_INVALID_ARGUMENT, "null handle"); \
+    NvtxRange nvtx_range_(__func__);                                    \
     try {                                                               \
       CK(cudaSetDevice((h)->device));                                   \
       __VA_ARGS__;                                                      \
@@ -2140,6 +2153,7 @@ int numpmp_gpu_transfer_bytes(const numpmp_gpu* h, int64_t* h2d, int64_t* d2h) {
 
 void numpmp_gpu_destroy(numpmp_gpu* h) {
   if (!h) return;
+  NvtxRange nvtx_range_("numpmp_gpu_destroy");
   PhaseTimer pt;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
