@@ -56,9 +56,6 @@ namespace numpmp_dev {
 #ifndef NUMPMP_GATHER_UNROLL
 #define NUMPMP_GATHER_UNROLL 8
 #endif
-#ifndef NUMPMP_FLAT_GATHER
-#define NUMPMP_FLAT_GATHER 0
-#endif
 constexpr int kWarps = NUMPMP_WARPS;  // warps per block (gather passes)
 constexpr int kThreads = kWarps * 32;
 constexpr int kMinBlocks = NUMPMP_MIN_BLOCKS;  // resident blocks per SM the passes are built for
@@ -334,32 +331,6 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
       const int gp = nb + 4 * (lane + 32 * i);
       if (gp < span_end) buf[i] = ld_stream_int4(idx + gp, pol_stream);
     }
-#if NUMPMP_FLAT_GATHER
-    // Flat gathers: the round's entries are gathered lane-strided (entry
-    // h + lane + 32u), kUnroll per lane, so every lane of every gather
-    // instruction is busy whatever the segment lengths, parked in shared
-    // memory, and each lane then sums its own segment from there in index
-    // order -- the same additions in the same order as the per-lane form.
-    {
-      __shared__ double sval_all[kWarps][32 * kUnroll];
-      double* sval = sval_all[threadIdx.x >> 5];
-      for (int hb = cb; hb < c1; hb += 32 * kUnroll) {
-        const int he = min(hb + 32 * kUnroll, c1);
-        double vv[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int e = hb + lane + 32 * u;
-          vv[u] = (e < he) ? g(sidx[e - cb]) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) sval[lane + 32 * u] = vv[u];
-        __syncwarp();
-        const int lo = max(seg_beg, hb), hi = min(seg_end, he);
-        for (int k = lo; k < hi; ++k) acc += sval[k - hb];
-        __syncwarp();
-      }
-    }
-#else
     const int lo = max(seg_beg, cb), hi = min(seg_end, c1);
     // Batches of kUnroll gathers, the last one predicated: a lane never has
     // fewer than min(kUnroll, remaining) gathers in flight (the passes are
@@ -372,7 +343,6 @@ __device__ __forceinline__ double warp_segments_sum(const int* __restrict__ idx,
       for (int u = 0; u < kUnroll; ++u)
         if (k + u < hi) acc += vv[u];
     }
-#endif
     __syncwarp();
     cb = nb;
   }
