@@ -168,6 +168,8 @@ def lib():
             )
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("NUMPMP_LIB") and not hasattr(L, name):
+                continue  # an older variant build (A/B against earlier rounds) lacks later entry points
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -363,39 +363,4 @@ __global__ void k_double_to_int(const double* __restrict__ in, long long count, 
     out[i] = static_cast<int>(in[i]);
 }
 
-// ------------------------------------- interleaved route tiles (K1 layout)
-// A column block's routes re-laid per 32-stream tile: entry i of lane k's
-// route at ix[(off[t] + i) * 32 + k], the tile padded to its longest route
-// (padding = link 0, never gathered).  One coalesced 128-byte load then
-// feeds one gather per lane, in route order, with no shared-memory staging.
-// off[t] (in rows of 32) is the exclusive scan of the tiles' longest routes.
-__global__ void k_ix_tile_rows(const int* __restrict__ col_ptr, long long s0, long long s1,
-                               unsigned* __restrict__ rows) {
-  const int lane = threadIdx.x & 31;
-  const long long ntiles = (s1 - s0 + 31) / 32;
-  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += wstride) {
-    const long long j = s0 + t * 32 + lane;
-    const int len = j < s1 ? col_ptr[j + 1] - col_ptr[j] : 0;
-    const unsigned mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(len));
-    if (lane == 0) rows[t] = mx;
-  }
-}
-__global__ void k_ix_fill(const int* __restrict__ col_ptr, const int* __restrict__ row_idx, long long s0,
-                          long long s1, const unsigned* __restrict__ off, int* __restrict__ ix) {
-  const int lane = threadIdx.x & 31;
-  const long long ntiles = (s1 - s0 + 31) / 32;
-  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += wstride) {
-    const long long j = s0 + t * 32 + lane;
-    const int beg = j < s1 ? col_ptr[j] : 0;
-    const int len = j < s1 ? col_ptr[j + 1] - beg : 0;
-    const unsigned r0 = off[t], r1 = off[t + 1];
-    for (unsigned r = r0; r < r1; ++r) {
-      const int i = static_cast<int>(r - r0);
-      ix[static_cast<long long>(r) * 32 + lane] = i < len ? row_idx[beg + i] : 0;
-    }
-  }
-}
-
 }  // namespace numpmp_dev

@@ -184,10 +184,6 @@ struct BlockArgs {
   // metadata and no scan
   int row_mode;
   int pair_tiles;      // k_stream_pass streams per lane (1 = tiles; 2 / 4 for short routes)
-  // interleaved route tiles (k_stream_pass_ix; null: staged form): entry i of
-  // lane k's route in tile t at ix[(ix_off[t] + i) * 32 + k]
-  const int* ix;
-  const unsigned* ix_off;
   const int* row_ptr;  // m+1 (this block's CSR)
   long long m;
   // split rows (> kSplitMin entries, e.g. the hot links of gen_congested)
@@ -221,11 +217,6 @@ __device__ __forceinline__ int4 ld_stream_int4(const int* p, uint64_t pol) {
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
       : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ int ld_stream_i32(const int* p, uint64_t pol) {
-  int r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
   return r;
 }
 __device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
@@ -658,90 +649,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a
     stream_pass_multi<kQ>(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   else
     stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
-  block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
-}
-
-// Interleaved route tiles (BlockArgs::ix): a warp's 32 streams read their
-// routes row by row, one coalesced 128-byte index load per row feeding one
-// gather per lane, the next batch's index rows in flight while the current
-// batch gathers.  Each route is summed in route order, as in the staged
-// form, so x is bit-identical; what goes is the chain offsets -> shuffle ->
-// 128-bit staging -> shared memory in front of every tile's first gather.
-// The tile's row range is loaded one tile ahead.
-#ifndef NUMPMP_IX_MINB
-#define NUMPMP_IX_MINB NUMPMP_MIN_BLOCKS
-#endif
-__global__ void __launch_bounds__(kThreads, NUMPMP_IX_MINB) k_stream_pass_ix(IterArgs a, BlockArgs bk) {
-  if (kernel_should_exit(a.ctrl)) return;
-  const double rho = a.ctrl->rho;
-  const long long kk = a.ctrl->run_k + 1;
-  const bool trace_it = (a.mode == MODE_RUN) && (kk % a.trace_every == 0);
-  const int sel = a.ctrl->v_sel;
-  const GatherV g{(sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1]};
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol_first = policy_evict_first();
-  const uint64_t pol_last = policy_evict_last();
-  const long long ntiles = (bk.s1 - bk.s0 + 31) / 32;
-  const long long tstride = (long long)gridDim.x * kWarps;
-  const double alpha = a.alpha;
-  double p_tda2 = 0.0, p_obj = 0.0;
-  long long tile = (long long)blockIdx.x * kWarps + wib;
-  unsigned r0 = 0, r1 = 0;
-  if (tile < ntiles) {
-    r0 = __ldg(bk.ix_off + tile);
-    r1 = __ldg(bk.ix_off + tile + 1);
-  }
-  for (; tile < ntiles; tile += tstride) {
-    const long long j = bk.s0 + tile * 32 + lane;
-    const bool valid = j < bk.s1;
-    const int nr = static_cast<int>(r1 - r0);
-    const int* base = bk.ix + static_cast<long long>(r0) * 32 + lane;
-    int id[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) id[u] = (u < nr) ? ld_stream_i32(base + 32 * u, pol_first) : 0;
-    const int beg = __ldg(a.col_ptr + (valid ? j : bk.s1));
-    const int end = __ldg(a.col_ptr + (valid ? j + 1 : bk.s1));
-    double A = 0.0, w = 0.0;
-    int kd = 0;
-    if (valid) {
-      A = ld_stream_f64(a.A_in + j, pol_first);
-      w = __ldg(a.w + j);
-      kd = __ldg(a.kind + j);
-    }
-    if (tile + tstride < ntiles) {  // next tile's row range
-      r0 = __ldg(bk.ix_off + tile + tstride);
-      r1 = __ldg(bk.ix_off + tile + tstride + 1);
-    }
-    const int len = end - beg;
-    double sum = 0.0;
-    for (int k = 0; k < nr; k += kUnroll) {
-      int nid[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        nid[u] = (k + kUnroll + u < nr) ? ld_stream_i32(base + 32 * (k + kUnroll + u), pol_first) : 0;
-      double vv[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) vv[u] = (k + u < len) ? g(id[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (k + u < len) sum += vv[u];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) id[u] = nid[u];
-    }
-    asm volatile("" : "+r"(kd), "+d"(w) : : "memory");
-    if (valid) {
-      const double zeta = static_cast<double>(len) * A - sum;
-      const double x = (kd == NUMPMP_KIND_LOG) ? prox_log(zeta, w, rho, len)
-                                               : prox_linear_nonneg(zeta, w, rho, len);
-      const double An = alpha * x + (1.0 - alpha) * A;
-      const double dA = An - A;
-      st_hint_f64(a.x + j, x, pol_last);
-      st_hint_f64(a.A_out + j, An, pol_first);
-      p_tda2 += static_cast<double>(len) * dA * dA;
-      if (trace_it) p_obj += (kd == NUMPMP_KIND_LOG) ? w * log(x) : w * x;
-    }
-  }
-  double part[2] = {p_tda2, p_obj};
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 

@@ -251,8 +251,6 @@ struct ColBlock {
   int seg = 0;                // max entries per segment
   int row_mode = 0;           // k_link_pass in row mode (longest row short, see BlockArgs)
   int pair_tiles = 0;         // k_stream_pass on pair tiles (short routes, see BlockArgs)
-  int* ix = nullptr;          // interleaved route tiles (k_stream_pass_ix; BlockArgs::ix)
-  unsigned* ix_off = nullptr; // ntiles+1: first row of each tile
 };
 
 }  // namespace
@@ -468,8 +466,6 @@ BlockArgs block_args(const numpmp_gpu* h, int b) {
   k.first = b == 0;
   k.row_mode = cb.row_mode;
   k.pair_tiles = cb.pair_tiles;
-  k.ix = cb.ix;
-  k.ix_off = cb.ix_off;
   k.row_ptr = cb.row_ptr;
   k.m = h->m;
   k.pieces = cb.pieces;
@@ -532,9 +528,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    if (bk.ix)
-      k_stream_pass_ix<<<h->grid1, kThreads, 0, s1>>>(a, bk);
-    else if (bk.pair_tiles == 4)
+    if (bk.pair_tiles == 4)
       k_stream_pass<4><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else if (bk.pair_tiles == 2)
       k_stream_pass<2><<<h->grid1, kThreads, 0, s1>>>(a, bk);
@@ -778,41 +772,6 @@ int choose_blocks(int64_t n) {
 // segment bound is kSeg, raised so that the longest row fits one warp unit
 // (32 segments); consecutive whole rows are then packed greedily into units
 // of <= 32 segments (host pass over the per-row segment counts).
-// Interleaved route tiles of one column block (k_ix_tile_rows / k_ix_fill,
-// pmp_aux.cuh): rows per tile = its longest route, exclusive scan -> ix_off.
-void build_interleaved(numpmp_gpu* h, ColBlock& cb, int64_t* bytes) {
-  const long long ntiles = (cb.s1 - cb.s0 + 31) / 32;
-  if (ntiles == 0) return;
-  double max_pad = 2.0;
-  if (const char* env = std::getenv("NUMPMP_IX_MAX_PAD")) max_pad = std::atof(env);
-  int64_t tmpb = 0;
-  unsigned* off = dalloc<unsigned>(static_cast<size_t>(ntiles) + 1, &tmpb, h->stream);
-  unsigned* rows = dalloc<unsigned>(static_cast<size_t>(ntiles) + 1, &tmpb, h->stream);
-  CK(cudaMemsetAsync(rows + ntiles, 0, sizeof(unsigned), h->stream));
-  k_ix_tile_rows<<<grid_for(ntiles * 32), 256, 0, h->stream>>>(h->col_ptr, cb.s0, cb.s1, rows);
-  CK(cudaGetLastError());
-  size_t temp_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, rows, off, static_cast<int>(ntiles + 1), h->stream));
-  void* temp = nullptr;
-  CK(lib_malloc_async(&temp, temp_bytes > 0 ? temp_bytes : 1, h->stream));
-  CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, rows, off, static_cast<int>(ntiles + 1), h->stream));
-  unsigned total = 0;
-  CK(cudaMemcpyAsync(&total, off + ntiles, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  cudaFreeAsync(temp, h->stream);
-  cudaFreeAsync(rows, h->stream);
-  if (static_cast<double>(total) * 32.0 > max_pad * static_cast<double>(std::max<int64_t>(cb.nnz, 1))) {
-    cudaFreeAsync(off, h->stream);  // skewed route lengths: the staged form
-    return;
-  }
-  // the offsets move from the temporary count into the handle's accounting
-  cb.ix_off = off;
-  *bytes += static_cast<int64_t>(sizeof(unsigned)) * (ntiles + 1);
-  cb.ix = dalloc<int>(static_cast<size_t>(total) * 32 + kIdxPad, bytes, h->stream);
-  k_ix_fill<<<grid_for(ntiles * 32), 256, 0, h->stream>>>(h->col_ptr, h->row_idx, cb.s0, cb.s1, cb.ix_off, cb.ix);
-  CK(cudaGetLastError());
-}
-
 void segment_block(numpmp_gpu* h, ColBlock& cb) {
   const int64_t m = h->m;
   int64_t tmpb = 0;
@@ -943,8 +902,7 @@ void preload_kernels(int device) {
   if (device < 0 || device >= 64 || done[device]) return;
   std::vector<const void*> f;
 #define NUMPMP_K(k) f.push_back(reinterpret_cast<const void*>(&k))
-  NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>); NUMPMP_K(k_stream_pass_ix);
-  NUMPMP_K(k_ix_tile_rows); NUMPMP_K(k_ix_fill);
+  NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>);
   NUMPMP_K(k_link_epilogue<0>); NUMPMP_K(k_link_epilogue<1>);
   NUMPMP_K(k_refresh_v); NUMPMP_K(k_set_v); NUMPMP_K(k_residual_parts);
   NUMPMP_K(k_p2p_wait<0>); NUMPMP_K(k_p2p_epilogue<false>); NUMPMP_K(k_p2p_epilogue<true>); NUMPMP_K(k_p2p_finalize);
@@ -1068,14 +1026,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
 
   // Column blocks (stream ranges rounded to 32-stream tiles) and their CSRs.
   const int nbk = choose_blocks(n);
-  // NUMPMP_K1_IX=1: K1 on interleaved route tiles where the padding to each
-  // tile's longest route costs at most NUMPMP_IX_MAX_PAD x the block's
-  // nonzeros (default 2; C: 1.68).  Off by default: one 128-byte index load
-  // per gather row instead of one 512-byte load per 128 entries is +4.5% L1->L2
-  // requests, and the passes are request-bound: C K1 0.468 -> 0.490 ms, B
-  // -1.4% (profiles/r2_k1_interleaved_ab.txt)
-  bool k1_ix = false;
-  if (const char* env = std::getenv("NUMPMP_K1_IX")) k1_ix = std::atoi(env) != 0;
   CK(cudaMemsetAsync(h->deg, 0, sizeof(int) * static_cast<size_t>(m), h->stream));
   for (int k = 0; k < nbk; ++k) {
     ColBlock cb;
@@ -1099,7 +1049,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     k_add_degree<<<grid_for(m), 256, 0, h->stream>>>(cb.row_ptr, m, h->deg);
     CK(cudaGetLastError());
     segment_block(h, h->blocks.back());
-    if (h->blocks.back().pair_tiles == 1 && k1_ix) build_interleaved(h, h->blocks.back(), b);
   }
   CK(cudaStreamSynchronize(h->stream));
   pt.mark("create: device CSR build");
@@ -1109,11 +1058,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
-  for (const ColBlock& cb : h->blocks)
-    if (cb.ix) {  // the interleaved stream pass: its own occupancy
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass_ix, kThreads, 0));
-      break;
-    }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 2>, kThreads, 0));
   int occ3 = 0, occ2r = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
@@ -2187,8 +2131,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     for (void* p : {static_cast<void*>(cb.row_ptr), static_cast<void*>(cb.col_idx),
                     static_cast<void*>(cb.units), static_cast<void*>(cb.vptr),
                     static_cast<void*>(cb.vrow), static_cast<void*>(cb.pieces),
-                    static_cast<void*>(cb.uctr), static_cast<void*>(cb.upart),
-                    static_cast<void*>(cb.ix), static_cast<void*>(cb.ix_off)})
+                    static_cast<void*>(cb.uctr), static_cast<void*>(cb.upart)})
       bufs.push_back(p);
   for (void* p : bufs)  // back to the (retained) stream-ordered pool
     if (p) {

@@ -970,32 +970,6 @@ def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restate
         assert ok, err
 
 
-@pytest.mark.parametrize("blocks", ["1", "3"])
-def test_interleaved_stream_pass_is_bit_identical_to_staged(blocks, restatement, oracle_mod, monkeypatch):
-    # k_stream_pass_ix (interleaved route tiles, BlockArgs::ix) sums every
-    # route in route order like the staged form: the whole solve must be
-    # bit-identical.  Ragged tail (n % 32 != 0), routes of 1..~25 links,
-    # 1 and 3 column blocks; NUMPMP_IX_MAX_PAD=1 forces the staged form.
-    monkeypatch.setenv("NUMPMP_COL_BLOCKS", blocks)
-    monkeypatch.setenv("NUMPMP_K1_IX", "1")
-    p = _gen(3000, 7001, 10.0, 2, True, 17)
-    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0)
-    sols = {}
-    for mode in ("ix", "staged"):
-        monkeypatch.setenv("NUMPMP_IX_MAX_PAD", "2" if mode == "ix" else "1")
-        with pmp.PmpSolver(p, cfg) as s:
-            sols[mode] = s.solve()
-    a, b = sols["ix"], sols["staged"]
-    assert a.iterations == b.iterations
-    np.testing.assert_array_equal(a.x, b.x)
-    np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
-    assert a.objective == b.objective and a.r_norm == b.r_norm and a.s_norm == b.s_norm
-    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
-    assert a.iterations == ref.iterations
-    ok, err = close(a.x, ref.x)
-    assert ok, err
-
-
 @pytest.mark.parametrize("pair_tau,tile_q", [("0", "2"), ("100", "2"), ("100", "4")])
 def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, tile_q, restatement, oracle_mod, monkeypatch):
     # the stream pass on 32-stream tiles and on multi-route tiles (2 or 4
