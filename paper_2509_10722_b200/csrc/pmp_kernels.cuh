@@ -281,9 +281,14 @@ struct GatherV {  // v_l (written by the previous link pass)
   const double* __restrict__ v;
   __device__ __forceinline__ double operator()(int l) const { return __ldg(v + l); }
 };
-struct GatherX {  // x_j (written by this iteration's stream pass)
+// x_j (written by this iteration's stream pass).  kL1: allocate in L1
+// (ld.global.nc) -- the row-mode link pass: P 0.574 -> 0.463 ms, C -1.1%;
+// warp units and pieces keep L1::no_allocate (B +0.6% with allocation),
+// profiles/r2_x_l1_alloc_ab.txt.
+template <bool kL1>
+struct GatherX {
   const double* __restrict__ x;
-  __device__ __forceinline__ double operator()(int j) const { return ld_gather_f64(x + j); }
+  __device__ __forceinline__ double operator()(int j) const { return kL1 ? __ldg(x + j) : ld_gather_f64(x + j); }
 };
 
 // Warp-cooperative segmented gather-sum.  The 32 lanes own contiguous,
@@ -925,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
       const int span_beg = __shfl_sync(kFull, rb, 0);
       const int span_end = __shfl_sync(kFull, re, 31);
       const double s = warp_segments_sum(bk.col_idx, span_beg, span_end, rb, re, sidx[wib], lane,
-                                         GatherX{src}, pol_first);
+                                         GatherX<true>{src}, pol_first);
       if (valid) row_done(r, bk.first ? s : Lprev + s);
     }
   } else {
@@ -949,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
       const int span_beg = __shfl_sync(kFull, vb, 0);
       const int span_end = __shfl_sync(kFull, ve, 31);
       double s = warp_segments_sum(bk.col_idx, span_beg, span_end, vb, ve, sidx[wib], lane,
-                                   GatherX{src}, pol_first);
+                                   GatherX<false>{src}, pol_first);
   #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {  // segmented scan, segments = equal rows
         const double t = __shfl_up_sync(kFull, s, d);
@@ -964,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, kForm == 0 ? NUMPMP_ROW_MINB : kMinB
     // split rows, piece by piece
     for (long long q = (long long)blockIdx.x * kWarps + wib; kForm == 2 && q < bk.npieces; q += ustride) {
       const int4 pc = ld_nc_int4(bk.pieces + q);
-      double s = warp_strided_sum(bk.col_idx, pc.x, pc.y, sidx[wib], lane, GatherX{src}, pol_first);
+      double s = warp_strided_sum(bk.col_idx, pc.x, pc.y, sidx[wib], lane, GatherX<false>{src}, pol_first);
   #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);  // same bits on every lane
       const int rb = __ldg(bk.row_ptr + pc.z), re = __ldg(bk.row_ptr + pc.z + 1);
