@@ -756,14 +756,25 @@ void check_view(const numpmp_problem_view* pv) {
 // Column blocking: x of one block should stay L2-resident between its
 // stream pass and its link-pass gather (126 MB L2, shared with the
 // streamed index and state arrays).  NUMPMP_COL_BLOCKS overrides.
-int choose_blocks(int64_t n) {
+int choose_blocks(int64_t n, int64_t m, int64_t nnz) {
   if (const char* env = std::getenv("NUMPMP_COL_BLOCKS")) {
     const int v = std::atoi(env);
     if (v >= 1) return static_cast<int>(std::min<int64_t>(v, std::max<int64_t>(1, n / 32)));
   }
   const int64_t xbytes = 8 * n;
+  // Every block after the first re-reads its CSR's row pointers and the
+  // accumulated loads (4 + 2 x 8 bytes per link).  When that is as large as x
+  // itself, keeping x L2-resident costs more than it saves: the paper shape P
+  // (10M links, 5M streams) runs 0.745 ms/iteration in one block against
+  // 0.798 in two (profiles/r2_col_blocks_sweep.txt).
+  if (20 * m >= xbytes) return 1;
   const int64_t target = 24ll << 20;
   int64_t nb = (xbytes + target - 1) / target;
+  // ... and no block below ~12.5M nonzeros: each block's two launches (their
+  // tails, the per-block row pass) are a fixed cost, and short routes make
+  // the blocks of the transit instance E light (51.7M nonzeros: 6 blocks by
+  // x alone 0.373 ms/iteration, 4 blocks 0.361; C keeps 4)
+  nb = std::min<int64_t>(nb, std::max<int64_t>(1, nnz / 12500000));
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, 16));
   return static_cast<int>(std::min<int64_t>(nb, std::max<int64_t>(1, n / 32)));
 }
@@ -1025,7 +1036,7 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   pt.mark("create: device validation");
 
   // Column blocks (stream ranges rounded to 32-stream tiles) and their CSRs.
-  const int nbk = choose_blocks(n);
+  const int nbk = choose_blocks(n, m, nnz);
   CK(cudaMemsetAsync(h->deg, 0, sizeof(int) * static_cast<size_t>(m), h->stream));
   for (int k = 0; k < nbk; ++k) {
     ColBlock cb;

@@ -9,7 +9,7 @@ timeout 180 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 2400 python -m pytest tests/ -q -m gpu -s > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 600 ./build/test_dropin > gpurun_out/dropin_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/dropin_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_C_$TAG.json 2> gpurun_out/bench_C_$TAG.err
-for c in B E D; do
+for c in B E D P; do
   timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_$TAG.json 2> gpurun_out/bench_${c}_$TAG.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_stream_pass|k_link_pass|k_link_epilogue" -s 10 -c 9 -o gpurun_out/prof_c_$TAG -f python scripts/profile_run.py C 6 > gpurun_out/ncu_full_$TAG.log 2>&1
 for c in B C; do timeout 600 python scripts/bench_p2p_overhead.py --config $c --steps 3 >> gpurun_out/p2p_overhead_$TAG.jsonl 2>>gpurun_out/p2p_overhead_$TAG.err; done
 tail -n 3 gpurun_out/smoke_$TAG.log gpurun_out/pytest_gpu_$TAG.log; tail -n 2 gpurun_out/dropin_$TAG.log
-for c in C B E D; do python -c "
+for c in C B E D P; do python -c "
 import json
 d=json.loads(open('gpurun_out/bench_${c}_$TAG.json').read().strip().splitlines()[-1])
 r=d['iteration_roofline']
