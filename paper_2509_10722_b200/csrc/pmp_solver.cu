@@ -933,9 +933,13 @@ void preload_kernels(int device) {
   preload_link_pass<LP_GATHER>(f);
   preload_link_pass<LP_ROWSUM>(f);
   preload_link_pass<LP_P2P>(f);
+  // NUMPMP_CARVEOUT=<percent>: shared-memory carveout preference for every
+  // kernel (A/B of the L1 share the gathered vectors get; unset: driver default)
+  const char* carve = std::getenv("NUMPMP_CARVEOUT");
   for (const void* fn : f) {
     cudaFuncAttributes attr;
     CK(cudaFuncGetAttributes(&attr, fn));
+    if (carve) CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(carve)));
   }
   done[device] = true;
 }
