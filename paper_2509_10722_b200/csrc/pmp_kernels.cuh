@@ -639,8 +639,11 @@ __device__ __forceinline__ void stream_pass_multi(const IterArgs& a, const Block
 
 // kQ: streams per lane (1: 32-stream tiles; 2 / 4: multi-route tiles for
 // short routes) -- separate instantiations, each with its own registers.
+#ifndef NUMPMP_Q_MINB
+#define NUMPMP_Q_MINB NUMPMP_MIN_BLOCKS  // resident CTAs per SM the multi-route tiles are built for
+#endif
 template <int kQ>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
+__global__ void __launch_bounds__(kThreads, kQ > 1 ? NUMPMP_Q_MINB : kMinBlocks) k_stream_pass(IterArgs a, BlockArgs bk) {
   __shared__ __align__(16) int sidx[kWarps][kQ > 1 ? kStageQ : kStageInts];
   if (kernel_should_exit(a.ctrl)) return;
   const double rho = a.ctrl->rho;

@@ -1072,7 +1072,11 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   int occ1 = 0, occ2 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass<1>, kThreads, 0));
+  {  // the stream pass of the blocks' tile form (multi-route tiles have their own launch bound)
+    const int q0 = h->blocks.empty() ? 1 : h->blocks.front().pair_tiles;
+    void (*k1)(IterArgs, BlockArgs) = q0 == 4 ? k_stream_pass<4> : q0 == 2 ? k_stream_pass<2> : k_stream_pass<1>;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, kThreads, 0));
+  }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 2>, kThreads, 0));
   int occ3 = 0, occ2r = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_link_epilogue<0>, kThreads, 0));
