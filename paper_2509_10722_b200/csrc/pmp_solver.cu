@@ -1283,8 +1283,12 @@ void p2p_wire(numpmp_gpu* h, const std::vector<void*>& bases) {
   for (size_t q = 0; q < W; ++q) {
     if (static_cast<int>(q) == h->rank) continue;
     cudaPointerAttributes at{};
-    CK(cudaPointerGetAttributes(&at, bases[q]));
-    if (at.device == h->device) distinct = false;
+    if (cudaPointerGetAttributes(&at, bases[q]) != cudaSuccess) {
+      cudaGetLastError();  // unknown placement: keep the form that is safe on a shared GPU
+      distinct = false;
+    } else if (at.device == h->device) {
+      distinct = false;
+    }
   }
   h->p2p_fused = distinct;
   // A/B: 0 off, 1 on where no rank shares this GPU; 2 on regardless (tests
