@@ -363,15 +363,4 @@ __global__ void k_double_to_int(const double* __restrict__ in, long long count, 
     out[i] = static_cast<int>(in[i]);
 }
 
-// Route entries for k_stream_pass_hot: -1 - slot for a hot link, else the link.
-__global__ void k_hot_index(const int* __restrict__ row_idx, long long nnz, const int* __restrict__ hot_slot,
-                            int* __restrict__ hidx) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nnz;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int l = row_idx[t];
-    const int s = hot_slot[l];
-    hidx[t] = s >= 0 ? -1 - s : l;
-  }
-}
-
 }  // namespace numpmp_dev

@@ -165,16 +165,6 @@ struct IterArgs {
   P2PArgs p2p;
 };
 
-// Hot links (k_stream_pass_hot, its own kernel parameter so that IterArgs /
-// BlockArgs -- and with them the other kernels' code -- stay as they are):
-// route entries of the nhot highest-degree links encoded as -1 - slot in
-// hidx (else the link id), their v cached in shared memory per CTA.
-struct HotArgs {
-  const int* hidx;
-  const int* hot_links;
-  int nhot;
-};
-
 // One column block: streams [s0, s1), the CSR of their columns, and its
 // segmentation into segments of at most `seg` consecutive entries of one
 // link (rows split evenly), packed into warp units of <= 32 segments of
@@ -539,7 +529,7 @@ __global__ void __launch_bounds__(256) k_set_v(IterArgs a) {
 template <class G>
 __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockArgs& bk, G g,
                                                  double rho, bool trace_it, int* sidx,
-                                                 double& p_tda2, double& p_obj, const int* idx) {
+                                                 double& p_tda2, double& p_obj) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol_first = policy_evict_first();
   const uint64_t pol_last = policy_evict_last();
@@ -562,7 +552,8 @@ __device__ __forceinline__ void stream_pass_body(const IterArgs& a, const BlockA
     }
     const int span_beg = __shfl_sync(kFull, beg, 0);
     const int span_end = __shfl_sync(kFull, end, 31);
-    const double sum = warp_segments_sum(idx, span_beg, span_end, beg, end, sidx, lane, g, pol_first);
+    const double sum = warp_segments_sum(a.row_idx, span_beg, span_end, beg, end, sidx, lane, g,
+                                         pol_first);
     // keep the kind test (and with it the wait for the kind / weight loads)
     // after the gather loop: the compiler otherwise hoists it and the warp
     // stalls on those loads before issuing any gather
@@ -665,35 +656,7 @@ __global__ void __launch_bounds__(kThreads, kQ > 1 ? NUMPMP_Q_MINB : kMinBlocks)
   if (kQ > 1)
     stream_pass_multi<kQ>(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   else
-    stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1], a.row_idx);
-  block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
-}
-
-// Stream pass with the hot links' v in shared memory (congested instances:
-// config G's ~100 hot links per route all gather from the same 1000 values,
-// which L1 serves at about one wavefront per distinct line -- ~25 per gather
-// instruction; shared memory serves them at its bank-conflict degree).  The
-// route entries come from hidx (-1 - slot for a hot link), so every route is
-// still summed in route order: bit-identical to k_stream_pass<1>.
-constexpr int kHotMax = 2048;
-struct GatherVHot {
-  const double* __restrict__ v;
-  const double* sv;  // shared: v of the hot links, by slot
-  __device__ __forceinline__ double operator()(int l) const { return l >= 0 ? __ldg(v + l) : sv[-1 - l]; }
-};
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_stream_pass_hot(IterArgs a, BlockArgs bk, HotArgs hot) {
-  __shared__ __align__(16) int sidx[kWarps][kStageInts];
-  __shared__ double sv[kHotMax];
-  if (kernel_should_exit(a.ctrl)) return;
-  const double rho = a.ctrl->rho;
-  const long long k = a.ctrl->run_k + 1;
-  const bool trace_it = (a.mode == MODE_RUN) && (k % a.trace_every == 0);
-  double part[2] = {0.0, 0.0};
-  const int sel = a.ctrl->v_sel;
-  const double* v = (sel == 0 || a.v_alt[0] == nullptr) ? a.v : a.v_alt[sel - 1];
-  for (int s = threadIdx.x; s < hot.nhot; s += blockDim.x) sv[s] = __ldg(v + __ldg(hot.hot_links + s));
-  __syncthreads();
-  stream_pass_body(a, bk, GatherVHot{v, sv}, rho, trace_it, sidx[threadIdx.x >> 5], part[0], part[1], hot.hidx);
+    stream_pass_body(a, bk, GatherV{v}, rho, trace_it, sb, part[0], part[1]);
   block_sum_store<2>(part, a.k1_part + 2 * ((long long)bk.index * a.grid1 + blockIdx.x));
 }
 

@@ -262,9 +262,6 @@ struct numpmp_gpu {
   cudaEvent_t pipe_ev[2 * kMaxBlocks + 2] = {};
   bool split_epilogue = true;      // NUMPMP_SPLIT_EPILOGUE=0: epilogue fused into the last link pass
   bool pipeline = true;            // NUMPMP_PIPELINE=0: serial graph (K1(b+1) no longer overlaps K2(b))
-  int* hidx = nullptr;             // nnz: route entries with hot links as -1 - slot (k_stream_pass_hot)
-  int* hot_links = nullptr;        // nhot: the hot links, by slot
-  int nhot = 0;
   std::string err;
   numpmp_config cfg{};
   int64_t m = 0, n = 0, nnz = 0;
@@ -531,9 +528,7 @@ void enqueue_iteration(numpmp_gpu* h, int parity, int mode, cudaEvent_t* ev, boo
     const BlockArgs bk = block_args(h, b);
     cudaStream_t s1 = pipelined ? h->stream2 : h->stream;
     if (pipelined && b >= 2) CK(cudaStreamWaitEvent(h->stream2, ev_k2[b - 2], 0));
-    if (h->nhot > 0 && bk.pair_tiles == 1)
-      k_stream_pass_hot<<<h->grid1, kThreads, 0, s1>>>(a, bk, HotArgs{h->hidx, h->hot_links, h->nhot});
-    else if (bk.pair_tiles == 4)
+    if (bk.pair_tiles == 4)
       k_stream_pass<4><<<h->grid1, kThreads, 0, s1>>>(a, bk);
     else if (bk.pair_tiles == 2)
       k_stream_pass<2><<<h->grid1, kThreads, 0, s1>>>(a, bk);
@@ -761,40 +756,6 @@ void check_view(const numpmp_problem_view* pv) {
 // Column blocking: x of one block should stay L2-resident between its
 // stream pass and its link-pass gather (126 MB L2, shared with the
 // streamed index and state arrays).  NUMPMP_COL_BLOCKS overrides.
-// Hot links (k_stream_pass_hot): links of degree >= max(1024, 16 x the
-// mean), the kHotMax highest, get their v cached in shared memory by the
-// stream pass.  Only congested instances have any (G: the 1000 hot links of
-// gen_congested, ~100 per route).  NUMPMP_HOT=0 disables.
-void build_hot_links(numpmp_gpu* h) {
-  if (const char* env = std::getenv("NUMPMP_HOT"))
-    if (std::atoi(env) == 0) return;
-  const int64_t m = h->m, nnz = h->nnz;
-  if (m == 0 || nnz == 0) return;
-  std::vector<int> deg(static_cast<size_t>(m));
-  CK(cudaMemcpy(deg.data(), h->deg, sizeof(int) * static_cast<size_t>(m), cudaMemcpyDeviceToHost));
-  const double thr = std::max(1024.0, 16.0 * static_cast<double>(nnz) / static_cast<double>(m));
-  std::vector<int> hot;
-  for (int64_t l = 0; l < m; ++l)
-    if (static_cast<double>(deg[static_cast<size_t>(l)]) >= thr) hot.push_back(static_cast<int>(l));
-  if (hot.empty()) return;
-  std::stable_sort(hot.begin(), hot.end(), [&](int x, int y) { return deg[static_cast<size_t>(x)] > deg[static_cast<size_t>(y)]; });
-  if (hot.size() > static_cast<size_t>(kHotMax)) hot.resize(static_cast<size_t>(kHotMax));
-  std::vector<int> slot(static_cast<size_t>(m), -1);
-  for (size_t s = 0; s < hot.size(); ++s) slot[static_cast<size_t>(hot[s])] = static_cast<int>(s);
-  int64_t tmpb = 0;
-  int* dslot = dalloc<int>(static_cast<size_t>(m), &tmpb, h->stream);
-  CK(cudaMemcpyAsync(dslot, slot.data(), sizeof(int) * static_cast<size_t>(m), cudaMemcpyHostToDevice, h->stream));
-  h->hot_links = dalloc<int>(hot.size(), &h->dev_bytes, h->stream);
-  CK(cudaMemcpyAsync(h->hot_links, hot.data(), sizeof(int) * hot.size(), cudaMemcpyHostToDevice, h->stream));
-  h->hidx = dalloc<int>(static_cast<size_t>(nnz) + kIdxPad, &h->dev_bytes, h->stream);
-  CK(cudaMemsetAsync(h->hidx + nnz, 0, sizeof(int) * kIdxPad, h->stream));
-  k_hot_index<<<grid_for(nnz), 256, 0, h->stream>>>(h->row_idx, nnz, dslot, h->hidx);
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(h->stream));  // the host slot table dies here
-  cudaFreeAsync(dslot, h->stream);
-  h->nhot = static_cast<int>(hot.size());
-}
-
 int choose_blocks(int64_t n, int64_t m, int64_t nnz) {
   if (const char* env = std::getenv("NUMPMP_COL_BLOCKS")) {
     const int v = std::atoi(env);
@@ -953,7 +914,6 @@ void preload_kernels(int device) {
   std::vector<const void*> f;
 #define NUMPMP_K(k) f.push_back(reinterpret_cast<const void*>(&k))
   NUMPMP_K(k_stream_pass<1>); NUMPMP_K(k_stream_pass<2>); NUMPMP_K(k_stream_pass<4>);
-  NUMPMP_K(k_stream_pass_hot); NUMPMP_K(k_hot_index);
   NUMPMP_K(k_link_epilogue<0>); NUMPMP_K(k_link_epilogue<1>);
   NUMPMP_K(k_refresh_v); NUMPMP_K(k_set_v); NUMPMP_K(k_residual_parts);
   NUMPMP_K(k_p2p_wait<0>); NUMPMP_K(k_p2p_epilogue<false>); NUMPMP_K(k_p2p_epilogue<true>); NUMPMP_K(k_p2p_finalize);
@@ -1106,7 +1066,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     segment_block(h, h->blocks.back());
   }
   CK(cudaStreamSynchronize(h->stream));
-  build_hot_links(h);
   pt.mark("create: device CSR build");
 
   // Persistent grids: resident blocks x SMs.
@@ -1117,7 +1076,6 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
     const int q0 = h->blocks.empty() ? 1 : h->blocks.front().pair_tiles;
     void (*k1)(IterArgs, BlockArgs) = q0 == 4 ? k_stream_pass<4> : q0 == 2 ? k_stream_pass<2> : k_stream_pass<1>;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, kThreads, 0));
-    if (h->nhot > 0 && q0 == 1) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stream_pass_hot, kThreads, 0));
   }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_link_pass<LP_FUSED, 2>, kThreads, 0));
   int occ3 = 0, occ2r = 0;
@@ -2172,8 +2130,7 @@ void numpmp_gpu_destroy(numpmp_gpu* h) {
     cudaFree(h->xregion);
     h->v = h->v_alt[0] = h->v_alt[1] = nullptr;  // lived in the exchange region
   }
-  std::vector<void*> bufs = {h->hidx,    h->hot_links,
-                             h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
+  std::vector<void*> bufs = {h->col_ptr, h->row_idx, h->w,         h->kind,       h->deg,
                              h->cap,     h->x,       h->v,         h->ps0,        h->pbar0,
                              h->done_cnt, h->ep_part, h->peer_tables,
                              h->v_alt[0], h->v_alt[1],

@@ -970,32 +970,6 @@ def test_link_pass_row_and_unit_modes_match_oracle(row_mode_max, blocks, restate
         assert ok, err
 
 
-def test_hot_link_stream_pass_is_bit_identical(restatement, oracle_mod, monkeypatch):
-    # k_stream_pass_hot (congested instances: the hot links' v in shared
-    # memory, route entries re-encoded) sums every route in route order like
-    # k_stream_pass<1>: the whole solve must be bit-identical, and match the
-    # oracle.  4 hot links on 40% of 20000 streams (degree 8000 >= the
-    # max(1024, 16 x mean) threshold), 2 column blocks.
-    monkeypatch.setenv("NUMPMP_COL_BLOCKS", "2")
-    spec = pmp.GenSpec(m=400, n=20000, avg_links_per_stream=5.0, kind=pmp.GenKind.Mixed,
-                       weights=pmp.WeightDist.uniform(0.5, 1.5), seed=9)
-    p = pmp.gen_congested(spec, 0.01, 0.4)
-    cfg = pmp.SolverConfig(eps_abs=1e-5, rho0=1000.0, max_iters=3000)
-    sols = {}
-    for hot in ("1", "0"):
-        monkeypatch.setenv("NUMPMP_HOT", hot)
-        with pmp.PmpSolver(p, cfg) as s:
-            sols[hot] = s.solve()
-    a, b = sols["1"], sols["0"]
-    assert a.iterations == b.iterations
-    np.testing.assert_array_equal(a.x, b.x)
-    np.testing.assert_array_equal(a.lambda_raw, b.lambda_raw)
-    ref = restatement.solve(oracle_mod.arrays_from(p), ocfg(oracle_mod, cfg))
-    assert a.iterations == ref.iterations
-    ok, err = close(a.x, ref.x)
-    assert ok, err
-
-
 @pytest.mark.parametrize("pair_tau,tile_q", [("0", "2"), ("100", "2"), ("100", "4")])
 def test_stream_pass_tiles_and_pair_tiles_match_oracle(pair_tau, tile_q, restatement, oracle_mod, monkeypatch):
     # the stream pass on 32-stream tiles and on multi-route tiles (2 or 4
