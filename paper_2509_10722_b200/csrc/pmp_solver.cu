@@ -1094,8 +1094,10 @@ void create_common(numpmp_gpu* h, const numpmp_problem_view* pv) {
       1LL, std::min<long long>((tiles1 + kWarps - 1) / kWarps, gmult * sms * std::max(occ1, 1))));
   h->grid2 = static_cast<int>(std::max(
       1LL, std::min<long long>((tiles2 + kWarps - 1) / kWarps, gmult * sms * std::max(occ2, 1))));
+  long long emult = 1;  // NUMPMP_EPI_GRID_MULT: link-epilogue grid, x the resident CTAs (A/B)
+  if (const char* env = std::getenv("NUMPMP_EPI_GRID_MULT")) emult = std::max(1, std::atoi(env));
   h->grid3 = static_cast<int>(std::max(
-      1LL, std::min<long long>((m + kThreads - 1) / kThreads, 1LL * sms * std::max(occ3, 1))));
+      1LL, std::min<long long>((m + kThreads - 1) / kThreads, emult * sms * std::max(occ3, 1))));
   h->grid2r = static_cast<int>(std::max(
       1LL, std::min<long long>(((m + 31) / 32 + kWarps - 1) / kWarps, gmult * sms * std::max(occ2r, 1))));
   h->k1_part = dalloc<double>(2 * static_cast<size_t>(nbk) * static_cast<size_t>(h->grid1) +
